@@ -1,0 +1,208 @@
+/*
+ * collsim_b200.h -- C ABI of the B200-native gradient-aggregation hot path
+ * (KvStore init/push/pull/barrier -> dependency engine -> collectives ->
+ * SGD update) of arXiv 1802.06949, as modelled by the reference simulator
+ * `collsim` (R = /root/reference/proj).
+ *
+ * Conventions
+ *   - Every entry point returns an int status: 0 = ok, negative = error.
+ *     Codes -1..-5 mirror collsim::Error::Kind (R/core/include/collsim/error.hpp:10-31);
+ *     cs_last_error() returns the thread-local message of the last failure.
+ *     No C++ exception ever crosses this boundary.
+ *   - The caller owns every data pointer.  Device work is stream-ordered on
+ *     the cs_stream_t given (a cudaStream_t) or on an engine lane stream.
+ *   - Tags, ops and communicators are plain integers, as in the reference.
+ *
+ * Reference interfaces each group replaces (drop-in map):
+ *   kernels   <- tensor.cpp:61-64 copy (a), collective.cpp:228-236 rank-order
+ *                sum (b), model.cpp:17-27 sgd_update (c)
+ *   engine    <- engine.hpp:46-69  Engine{new_variable,push,wait_for,wait_all,shutdown}
+ *   transport <- collective.hpp:38-59 Transport{new_communicator,allreduce_sum,broadcast,barrier,set_inject_latency}
+ *   kvstore   <- kvstore.hpp:35-78 create_communicators, KvStore{init,push,pull,barrier,comm_buf,outstanding_in_flight}
+ *   trace     <- trace.hpp:14-78 TraceSink{emit,snapshot,write_jsonl}
+ *   trainer   <- trainer.cpp:89-151 train_epoch loop shapes (synthetic producer)
+ */
+#ifndef COLLSIM_B200_H_
+#define COLLSIM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cs_stream_t; /* == cudaStream_t */
+
+/* ------------------------------------------------------------ status */
+enum {
+  CS_OK = 0,
+  CS_ERR_CONFIG = -1,   /* collsim::ConfigError   */
+  CS_ERR_USAGE = -2,    /* collsim::UsageError    */
+  CS_ERR_MISMATCH = -3, /* collsim::MismatchError */
+  CS_ERR_DEADLOCK = -4, /* collsim::DeadlockTimeout */
+  CS_ERR_ENGINE = -5,   /* collsim::EngineError   */
+  CS_ERR_CUDA = -6,
+  CS_ERR_NCCL = -7,
+  CS_ERR_INTERNAL = -8
+};
+
+typedef enum cs_dtype { CS_F64 = 0, CS_F32 = 1, CS_BF16 = 2 } cs_dtype;
+
+const char* cs_last_error(void);
+const char* cs_status_name(int status); /* "ConfigError", ... (error.hpp:19-28) */
+int cs_version(void);
+int cs_device_count(int* out);
+
+/* ------------------------------------------------ kernels (a) (b) (c) */
+
+/* (a) pack / cast: dst[i] = (dst_dt) src[i] for every entry.  Used for the
+ * gradient -> comm-bucket staging copy (kvstore.cpp:109 `copy(g, comm_buf)`)
+ * and for the pull copy-out (kvstore.cpp:160/170). One launch per table. */
+typedef struct cs_copy_entry {
+  const void* src;
+  void* dst;
+  uint64_t n; /* elements */
+} cs_copy_entry;
+int cs_pack(const cs_copy_entry* entries, int n_entries, cs_dtype src_dt, cs_dtype dst_dt,
+            cs_stream_t stream);
+
+/* (b) multi-buffer rank-order sum: every out[j][i] = ((in[0][i] + in[1][i]) + ...) + in[m-1][i]
+ * (collective.cpp:228-236).  out[j] may alias in[j] (in-place allreduce).
+ * m, nout <= CS_MAX_RANKS.  Pointers may be peer (UVA) addresses. */
+#define CS_MAX_RANKS 16
+int cs_sum_buffers(const void* const* in, int m, void* const* out, int nout, uint64_t n,
+                   cs_dtype dt, cs_stream_t stream);
+
+/* (c) fused SGD / momentum update reading the reduced gradient directly:
+ *   momentum == 0: w[i] -= (lr*rescale) * g[i]              (model.cpp:17-27)
+ *   momentum  > 0: v = mu*v - (lr*rescale)*g; w += v        (MXNet form, new)
+ * w_dt in {F64,F32,BF16}; g_dt the comm dtype; mom has w's compute type
+ * (f64 for F64 weights, f32 otherwise) and may be NULL when momentum == 0. */
+typedef struct cs_update_entry {
+  void* w;
+  const void* g;
+  void* mom;
+  uint64_t n;
+} cs_update_entry;
+int cs_sgd_update(const cs_update_entry* entries, int n_entries, cs_dtype w_dt, cs_dtype g_dt,
+                  double lr, double rescale, double momentum, cs_stream_t stream);
+
+/* synthetic backward producer: dst = src (cast), then the kernel is held for
+ * at least spin_ns on the device (models per-key backward compute). */
+int cs_synth_backward(const void* src, void* dst, uint64_t n, cs_dtype dt, uint64_t spin_ns,
+                      int ctas, cs_stream_t stream);
+
+/* deterministic fp64 checksum sum_i x[i] of a buffer into *out_dev (device f64). */
+int cs_checksum(const void* x, uint64_t n, cs_dtype dt, double* out_dev, cs_stream_t stream);
+
+/* ------------------------------------------------------------- trace */
+typedef struct cs_trace* cs_trace_t;
+int cs_trace_create(cs_trace_t* out);
+int cs_trace_destroy(cs_trace_t t);
+int cs_trace_count(cs_trace_t t, uint64_t* out);
+int cs_trace_write_jsonl(cs_trace_t t, const char* path);
+/* gauges (trace.hpp:29-55): max_open_collectives, compute_overlap */
+int cs_trace_gauges(cs_trace_t t, int* max_open_collectives, int* compute_overlap);
+
+/* ------------------------------------------------------------ engine */
+typedef struct cs_engine* cs_engine_t;
+enum { CS_OP_COMPUTE = 0, CS_OP_COPY = 1, CS_OP_COLLECTIVE = 2, CS_OP_OTHER = 3 }; /* engine.hpp:30 */
+enum { CS_DISPATCH_INLINE = 0, CS_DISPATCH_POOL = 1, CS_DISPATCH_HOST = 2 };
+typedef int (*cs_host_fn)(void* arg); /* non-zero return = body failure */
+typedef int (*cs_stream_fn)(void* arg, cs_stream_t stream);
+
+/* device < 0: host-only engine (host ops only; no CUDA calls). */
+int cs_engine_create(int num_worker_threads, int rank, int device, cs_trace_t trace,
+                     cs_engine_t* out);
+int cs_engine_destroy(cs_engine_t e);
+int cs_engine_new_variable(cs_engine_t e, uint64_t* tag);
+/* Reference semantics (engine.hpp:57-58): body runs once every earlier
+ * conflicting op on its tags has completed (device work included). */
+int cs_engine_push_host(cs_engine_t e, cs_host_fn fn, void* arg, const uint64_t* reads, int n_reads,
+                        const uint64_t* mutates, int n_mutates, int kind, int key, uint64_t* op_id);
+/* Stream op: body enqueues device work on `lane`'s stream after the engine
+ * has made that stream wait for the CUDA events of every conflicting op. */
+int cs_engine_push_stream(cs_engine_t e, cs_stream_fn fn, void* arg, const uint64_t* reads,
+                          int n_reads, const uint64_t* mutates, int n_mutates, int kind, int key,
+                          int lane, int dispatch, uint64_t* op_id);
+int cs_engine_wait_for(cs_engine_t e, uint64_t tag);
+int cs_engine_wait_all(cs_engine_t e);
+int cs_engine_shutdown(cs_engine_t e);
+int cs_engine_new_lane(cs_engine_t e, int priority, int* lane);
+int cs_engine_lane_stream(cs_engine_t e, int lane, cs_stream_t* out);
+int cs_engine_stats(cs_engine_t e, uint64_t* pushed, uint64_t* completed);
+int cs_engine_num_threads(cs_engine_t e, int* out);
+
+/* --------------------------------------------------------- transport */
+typedef struct cs_transport* cs_transport_t;
+/* In-process ranks (threads), buffers on one or several local GPUs; the last
+ * arriver reduces with kernel (b) in rank order (collective.cpp:228-236). */
+int cs_transport_create_local(int num_ranks, int watchdog_ms, cs_trace_t trace,
+                              cs_transport_t* out);
+/* One process per GPU: matching ledger in POSIX shared memory `name`
+ * (rank 0 creates it), data over NCCL (NVLink / NVSwitch). */
+int cs_transport_create_nccl(const char* name, int num_ranks, int rank, int device,
+                             int watchdog_ms, cs_trace_t trace, cs_transport_t* out);
+/* Host-only matching ledger (no data movement) for CPU tests of the
+ * matching / watchdog logic: in-process when name is NULL or "", else shm. */
+int cs_transport_create_ledger_only(const char* name, int num_ranks, int rank, int watchdog_ms,
+                                    cs_trace_t trace, cs_transport_t* out);
+int cs_transport_destroy(cs_transport_t t);
+int cs_transport_num_ranks(cs_transport_t t, int* out);
+int cs_transport_num_communicators(cs_transport_t t, int* out);
+int cs_transport_new_communicator(cs_transport_t t, int* comm);
+int cs_transport_set_inject_latency(cs_transport_t t, int64_t us);
+int cs_transport_abort(cs_transport_t t);
+int cs_allreduce_sum(cs_transport_t t, int comm, int rank, void* buf, uint64_t n, cs_dtype dt,
+                     int trace_key, cs_stream_t stream);
+int cs_broadcast(cs_transport_t t, int comm, int rank, int root, void* buf, uint64_t n,
+                 cs_dtype dt, int trace_key, cs_stream_t stream);
+int cs_barrier(cs_transport_t t, int comm, int rank, int trace_key, cs_stream_t stream);
+
+/* ----------------------------------------------------------- kvstore */
+typedef struct cs_kvstore* cs_kvstore_t;
+enum { CS_KV_FUNNEL = 0, CS_KV_DEPCHA = 1, CS_KV_CONCOM = 2, CS_KV_NAIVE = 3 }; /* kvstore.hpp:21 */
+typedef struct cs_kv_config {
+  int mode;              /* CS_KV_* */
+  int outstanding;       /* concom window / number of extra communicators */
+  int num_keys;
+  int comm_dtype;        /* cs_dtype of the comm buffers (-1: dtype of the init weights) */
+  uint64_t bucket_bytes; /* 0: one comm buffer per key (reference 1:1 map, kvstore.cpp:84) */
+  int issue_order;       /* bucket grouping order: 0 ascending keys, 1 descending */
+  int comm_priority;     /* CUDA stream priority of the comm lanes (<=0, lower = higher prio) */
+} cs_kv_config;
+typedef struct cs_slot { /* TensorSlot (kvstore.hpp:16-19): non-owning device view + tag */
+  void* data;
+  int dtype;
+  uint64_t numel;
+  uint64_t tag;
+} cs_slot;
+typedef struct cs_sgd {
+  double lr;
+  double rescale;
+  double momentum;
+} cs_sgd;
+int cs_create_communicators(cs_transport_t t, int count, int* comms_out); /* kvstore.hpp:35 */
+int cs_kv_create(cs_engine_t e, cs_transport_t t, int rank, const cs_kv_config* cfg,
+                 const int* concom_comms, int n_comms, cs_kvstore_t* out);
+int cs_kv_destroy(cs_kvstore_t kv);
+int cs_kv_init(cs_kvstore_t kv, int key, cs_slot weights);
+/* list forms (MXNet KVStore push/pull of key lists; n == 1 is the reference call) */
+int cs_kv_push(cs_kvstore_t kv, const int* keys, const cs_slot* grads, int n);
+int cs_kv_pull(cs_kvstore_t kv, const int* keys, const cs_slot* outs, int n);
+/* pull fused with the SGD update: weights <- sgd(weights, aggregated grad) */
+int cs_kv_pull_update(cs_kvstore_t kv, const int* keys, const cs_slot* weights, int n,
+                      const cs_sgd* sgd);
+int cs_kv_barrier(cs_kvstore_t kv);
+int cs_kv_outstanding_in_flight(cs_kvstore_t kv, int* out);
+/* synchronizes the key's comm buffer and copies it to host memory (comm dtype) */
+int cs_kv_comm_buf(cs_kvstore_t kv, int key, void* host_out, uint64_t* numel, int* dtype);
+int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems);
+int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
+int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLLSIM_B200_H_ */

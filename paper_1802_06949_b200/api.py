@@ -1,0 +1,475 @@
+"""Python mirror of the reference API over the C ABI.
+
+Names, argument meaning and error behaviour follow collsim
+(R/core/include/collsim/{engine,collective,kvstore,trace}.hpp) so the tests
+read like the reference's own tests:
+
+    Engine(num_worker_threads, rank=0, trace=None, device=-1)
+        .new_variable() / .push(body, reads, mutates, kind, key) / .wait_for(tag)
+        .wait_all() / .shutdown()
+    Transport.local(num_ranks, watchdog_ms, trace)      in-process ranks, kernel (b)
+    Transport.nccl(name, num_ranks, rank, device, ...)  one process per GPU
+        .allreduce_sum(comm, rank, buf, key, stream) / .broadcast / .barrier
+    KvStore(engine, transport, rank, KvConfig, concom_comms)
+        .init(key, slot) / .push(keys, slots) / .pull(keys, slots)
+        .pull_update(keys, slots, lr, rescale, momentum) / .barrier() / .comm_buf(key)
+
+Device buffers are torch tensors (plumbing only); everything they are handed
+to runs in libcollsim_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import tempfile
+import threading
+from dataclasses import dataclass
+from typing import Callable, Iterable, Sequence
+
+from . import _lib
+from ._lib import check, lib
+
+try:  # torch is plumbing: device memory and streams
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+F64, F32, BF16 = _lib.CS_F64, _lib.CS_F32, _lib.CS_BF16
+COMPUTE, COPY, COLLECTIVE, OTHER = 0, 1, 2, 3
+INLINE, POOL = _lib.CS_DISPATCH_INLINE, _lib.CS_DISPATCH_POOL
+MODES = {"funnel": 0, "depcha": 1, "concom": 2, "naive": 3}
+
+
+def dtype_code(dt) -> int:
+    if isinstance(dt, int):
+        return dt
+    if torch is not None:
+        if dt == torch.float64:
+            return F64
+        if dt == torch.float32:
+            return F32
+        if dt == torch.bfloat16:
+            return BF16
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def torch_dtype(code: int):
+    return {F64: torch.float64, F32: torch.float32, BF16: torch.bfloat16}[code]
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib.cs_device_count(C.byref(n)))
+    return n.value
+
+
+def _u64_array(xs: Sequence[int]):
+    arr = (C.c_uint64 * max(1, len(xs)))(*xs)
+    return arr, len(xs)
+
+
+# ------------------------------------------------------------------- trace
+
+class TraceSink:
+    """R/core/include/collsim/trace.hpp:57-78."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib.cs_trace_create(C.byref(h)))
+        self.h = h
+
+    def count(self) -> int:
+        n = C.c_uint64()
+        check(lib.cs_trace_count(self.h, C.byref(n)))
+        return n.value
+
+    def write_jsonl(self, path: str) -> None:
+        check(lib.cs_trace_write_jsonl(self.h, str(path).encode()))
+
+    def snapshot(self) -> list[dict]:
+        fd, path = tempfile.mkstemp(suffix=".jsonl")
+        os.close(fd)
+        try:
+            self.write_jsonl(path)
+            with open(path) as f:
+                return [json.loads(line) for line in f if line.strip()]
+        finally:
+            os.unlink(path)
+
+    def gauges(self) -> tuple[int, bool]:
+        a, b = C.c_int(), C.c_int()
+        check(lib.cs_trace_gauges(self.h, C.byref(a), C.byref(b)))
+        return a.value, bool(b.value)
+
+    def close(self):
+        if self.h:
+            lib.cs_trace_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ engine
+
+class Engine:
+    """Stream/event-mapped dependency engine (R/core/include/collsim/engine.hpp:41-74)."""
+
+    def __init__(self, num_worker_threads: int, rank: int = 0, trace: TraceSink | None = None,
+                 device: int = -1):
+        h = C.c_void_p()
+        check(lib.cs_engine_create(num_worker_threads, rank, device, trace.h if trace else None,
+                                   C.byref(h)))
+        self.h = h
+        self.device = device
+        self._keep: dict[int, object] = {}
+        self._keep_mu = threading.Lock()
+        self._next = 0
+
+    def new_variable(self) -> int:
+        t = C.c_uint64()
+        check(lib.cs_engine_new_variable(self.h, C.byref(t)))
+        return t.value
+
+    def _hold(self, obj) -> int:
+        with self._keep_mu:
+            self._next += 1
+            self._keep[self._next] = obj
+            return self._next
+
+    def _release(self, token: int) -> None:
+        with self._keep_mu:
+            self._keep.pop(token, None)
+
+    def push(self, body: Callable[[], None], reads: Iterable[int] = (), mutates: Iterable[int] = (),
+             kind: int = OTHER, key: int = -1) -> int:
+        """Host body, reference semantics: runs on the pool once every earlier
+        conflicting op has completed (device work included)."""
+        holder = {}
+
+        def tramp(_arg):
+            try:
+                body()
+                return 0
+            except BaseException:  # body failure poisons the engine
+                return 1
+            finally:
+                self._release(holder["t"])
+
+        cb = _lib.HOST_FN(tramp)
+        holder["t"] = self._hold(cb)
+        r, nr = _u64_array(list(reads))
+        m, nm = _u64_array(list(mutates))
+        op = C.c_uint64()
+        try:
+            check(lib.cs_engine_push_host(self.h, cb, None, r, nr, m, nm, kind, key, C.byref(op)))
+        except Exception:
+            self._release(holder["t"])
+            raise
+        return op.value
+
+    def push_stream(self, body: Callable[[int], None], reads: Iterable[int] = (),
+                    mutates: Iterable[int] = (), kind: int = OTHER, key: int = -1, lane: int = 0,
+                    dispatch: int = INLINE) -> int:
+        """Stream body: body(stream_handle) enqueues device work on the lane."""
+        holder = {}
+
+        def tramp(_arg, stream):
+            try:
+                body(stream or 0)
+                return 0
+            except BaseException:
+                return 1
+            finally:
+                self._release(holder["t"])
+
+        cb = _lib.STREAM_FN(tramp)
+        holder["t"] = self._hold(cb)
+        r, nr = _u64_array(list(reads))
+        m, nm = _u64_array(list(mutates))
+        op = C.c_uint64()
+        try:
+            check(lib.cs_engine_push_stream(self.h, cb, None, r, nr, m, nm, kind, key, lane, dispatch,
+                                            C.byref(op)))
+        except Exception:
+            self._release(holder["t"])
+            raise
+        return op.value
+
+    def wait_for(self, tag: int) -> None:
+        check(lib.cs_engine_wait_for(self.h, tag))
+
+    def wait_all(self) -> None:
+        check(lib.cs_engine_wait_all(self.h))
+
+    def shutdown(self) -> None:
+        check(lib.cs_engine_shutdown(self.h))
+
+    def new_lane(self, priority: int = 0) -> int:
+        lane = C.c_int()
+        check(lib.cs_engine_new_lane(self.h, priority, C.byref(lane)))
+        return lane.value
+
+    def lane_stream(self, lane: int = 0) -> int:
+        s = C.c_void_p()
+        check(lib.cs_engine_lane_stream(self.h, lane, C.byref(s)))
+        return s.value or 0
+
+    def num_threads(self) -> int:
+        n = C.c_int()
+        check(lib.cs_engine_num_threads(self.h, C.byref(n)))
+        return n.value
+
+    def stats(self) -> tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        check(lib.cs_engine_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self.h:
+            lib.cs_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------- transport
+
+def _buf_args(buf, dtype=None, count=None):
+    """(ptr, count, dtype) from a torch tensor or an explicit triple."""
+    if torch is not None and isinstance(buf, torch.Tensor):
+        return buf.data_ptr(), buf.numel(), dtype_code(buf.dtype)
+    return int(buf or 0), int(count or 0), dtype_code(dtype if dtype is not None else F32)
+
+
+class Transport:
+    """R/core/include/collsim/collective.hpp:36-61 over device memory."""
+
+    WORLD = 0
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @staticmethod
+    def world() -> int:
+        return 0
+
+    @classmethod
+    def local(cls, num_ranks: int, watchdog_ms: int = 5000, trace: TraceSink | None = None):
+        h = C.c_void_p()
+        check(lib.cs_transport_create_local(num_ranks, watchdog_ms, trace.h if trace else None,
+                                            C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def nccl(cls, name: str, num_ranks: int, rank: int, device: int, watchdog_ms: int = 60000,
+             trace: TraceSink | None = None):
+        h = C.c_void_p()
+        check(lib.cs_transport_create_nccl(name.encode(), num_ranks, rank, device, watchdog_ms,
+                                           trace.h if trace else None, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def ledger_only(cls, num_ranks: int, watchdog_ms: int = 5000, trace: TraceSink | None = None,
+                    name: str = "", rank: int = 0):
+        h = C.c_void_p()
+        check(lib.cs_transport_create_ledger_only(name.encode(), num_ranks, rank, watchdog_ms,
+                                                  trace.h if trace else None, C.byref(h)))
+        return cls(h)
+
+    def num_ranks(self) -> int:
+        n = C.c_int()
+        check(lib.cs_transport_num_ranks(self.h, C.byref(n)))
+        return n.value
+
+    def num_communicators(self) -> int:
+        n = C.c_int()
+        check(lib.cs_transport_num_communicators(self.h, C.byref(n)))
+        return n.value
+
+    def new_communicator(self) -> int:
+        c = C.c_int()
+        check(lib.cs_transport_new_communicator(self.h, C.byref(c)))
+        return c.value
+
+    def set_inject_latency(self, us: int) -> None:
+        check(lib.cs_transport_set_inject_latency(self.h, int(us)))
+
+    def abort(self) -> None:
+        check(lib.cs_transport_abort(self.h))
+
+    def allreduce_sum(self, comm: int, rank: int, buf, trace_key: int = -1, stream: int = 0,
+                      dtype=None, count=None) -> None:
+        p, n, dt = _buf_args(buf, dtype, count)
+        check(lib.cs_allreduce_sum(self.h, comm, rank, p, n, dt, trace_key, stream))
+
+    def broadcast(self, comm: int, rank: int, root: int, buf, trace_key: int = -1, stream: int = 0,
+                  dtype=None, count=None) -> None:
+        p, n, dt = _buf_args(buf, dtype, count)
+        check(lib.cs_broadcast(self.h, comm, rank, root, p, n, dt, trace_key, stream))
+
+    def barrier(self, comm: int, rank: int, trace_key: int = -1, stream: int = 0) -> None:
+        check(lib.cs_barrier(self.h, comm, rank, trace_key, stream))
+
+    def close(self):
+        if self.h:
+            lib.cs_transport_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def create_communicators(transport: Transport, count: int) -> list[int]:
+    """R/core/include/collsim/kvstore.hpp:32-35."""
+    arr = (C.c_int * max(1, count))()
+    check(lib.cs_create_communicators(transport.h, count, arr))
+    return list(arr[:count])
+
+
+# ----------------------------------------------------------------- kvstore
+
+@dataclass
+class KvConfig:
+    """R/core/include/collsim/kvstore.hpp:26-30 + B200 extensions."""
+    mode: str = "funnel"
+    outstanding: int = 1
+    num_keys: int = 0
+    comm_dtype: int = -1
+    bucket_bytes: int = 0
+    issue_order: int = 0
+    comm_priority: int = 0
+
+
+@dataclass
+class Slot:
+    """TensorSlot (kvstore.hpp:16-19): a device tensor plus its engine tag."""
+    value: "torch.Tensor"
+    tag: int
+
+    def c(self) -> _lib.SlotC:
+        return _lib.SlotC(self.value.data_ptr(), dtype_code(self.value.dtype), self.value.numel(),
+                          self.tag)
+
+
+class KvStore:
+    """Per-rank init/push/pull/barrier facade (R/core/include/collsim/kvstore.hpp:54-96)."""
+
+    def __init__(self, engine: Engine, transport: Transport, rank: int, config: KvConfig,
+                 concom_comms: Sequence[int] = ()):
+        cfg = _lib.KvConfigC(MODES[config.mode] if isinstance(config.mode, str) else config.mode,
+                             config.outstanding, config.num_keys, config.comm_dtype,
+                             config.bucket_bytes, config.issue_order, config.comm_priority)
+        comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
+        h = C.c_void_p()
+        check(lib.cs_kv_create(engine.h, transport.h, rank, C.byref(cfg), comms, len(concom_comms),
+                               C.byref(h)))
+        self.h = h
+        self.engine = engine
+        self.transport = transport
+        self.config = config
+        self.rank = rank
+
+    @staticmethod
+    def _lists(keys, slots):
+        if isinstance(keys, int):
+            keys, slots = [keys], [slots]
+        karr = (C.c_int * len(keys))(*keys)
+        sarr = (_lib.SlotC * len(slots))(*[s.c() for s in slots])
+        return karr, sarr, len(keys)
+
+    def init(self, key: int, weights: Slot) -> None:
+        check(lib.cs_kv_init(self.h, key, weights.c()))
+
+    def push(self, keys, grads) -> None:
+        k, s, n = self._lists(keys, grads)
+        check(lib.cs_kv_push(self.h, k, s, n))
+
+    def pull(self, keys, outs) -> None:
+        k, s, n = self._lists(keys, outs)
+        check(lib.cs_kv_pull(self.h, k, s, n))
+
+    def pull_update(self, keys, weights, lr: float, rescale: float, momentum: float = 0.0) -> None:
+        k, s, n = self._lists(keys, weights)
+        sgd = _lib.SgdC(lr, rescale, momentum)
+        check(lib.cs_kv_pull_update(self.h, k, s, n, C.byref(sgd)))
+
+    def barrier(self) -> None:
+        check(lib.cs_kv_barrier(self.h))
+
+    def outstanding_in_flight(self) -> int:
+        n = C.c_int()
+        check(lib.cs_kv_outstanding_in_flight(self.h, C.byref(n)))
+        return n.value
+
+    def comm_buf(self, key: int):
+        """Synchronizes and returns the key's comm buffer as a CPU tensor."""
+        n, dt = C.c_uint64(), C.c_int()
+        check(lib.cs_kv_comm_buf(self.h, key, None, C.byref(n), C.byref(dt)))
+        out = torch.empty(n.value, dtype=torch_dtype(dt.value))
+        check(lib.cs_kv_comm_buf(self.h, key, C.c_void_p(out.data_ptr()), None, None))
+        return out
+
+    def key_map(self, key: int) -> tuple[int, int]:
+        b, off = C.c_int(), C.c_uint64()
+        check(lib.cs_kv_key_map(self.h, key, C.byref(b), C.byref(off)))
+        return b.value, off.value
+
+    def num_buckets(self) -> int:
+        n = C.c_int()
+        check(lib.cs_kv_num_buckets(self.h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.h:
+            lib.cs_kv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------- kernels
+
+def pack(entries: Sequence[tuple], src_dt: int, dst_dt: int, stream: int = 0) -> None:
+    """Kernel (a): entries of (src_ptr, dst_ptr, n)."""
+    arr = (_lib.CopyEntry * max(1, len(entries)))(*[_lib.CopyEntry(s, d, n) for s, d, n in entries])
+    check(lib.cs_pack(arr, len(entries), src_dt, dst_dt, stream))
+
+
+def sum_buffers(ins: Sequence[int], outs: Sequence[int], n: int, dt: int, stream: int = 0) -> None:
+    """Kernel (b): every out = rank-order sum of ins."""
+    a = (C.c_void_p * max(1, len(ins)))(*ins)
+    b = (C.c_void_p * max(1, len(outs)))(*outs)
+    check(lib.cs_sum_buffers(a, len(ins), b, len(outs), n, dt, stream))
+
+
+def sgd_update(entries: Sequence[tuple], w_dt: int, g_dt: int, lr: float, rescale: float,
+               momentum: float = 0.0, stream: int = 0) -> None:
+    """Kernel (c): entries of (w_ptr, g_ptr, mom_ptr_or_0, n)."""
+    arr = (_lib.UpdateEntry * max(1, len(entries)))(
+        *[_lib.UpdateEntry(w, g, m or None, n) for w, g, m, n in entries])
+    check(lib.cs_sgd_update(arr, len(entries), w_dt, g_dt, lr, rescale, momentum, stream))
+
+
+def synth_backward(src: int, dst: int, n: int, dt: int, spin_ns: int = 0, ctas: int = 0,
+                   stream: int = 0) -> None:
+    check(lib.cs_synth_backward(src, dst, n, dt, spin_ns, ctas, stream))
+
+
+def checksum(x: int, n: int, dt: int, out_dev: int, stream: int = 0) -> None:
+    check(lib.cs_checksum(x, n, dt, out_dev, stream))

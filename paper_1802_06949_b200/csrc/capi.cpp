@@ -1,0 +1,453 @@
+// capi.cpp -- the extern "C" boundary (include/collsim_b200.h).  Every entry
+// point converts C++ exceptions into a status code + thread-local message;
+// nothing throws across the ABI.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "collsim_b200.h"
+#include "engine.hpp"
+#include "kernels.hpp"
+#include "kvstore.hpp"
+#include "transport.hpp"
+
+using namespace csb;
+
+struct cs_trace {
+  TraceSink sink;
+};
+struct cs_engine {
+  std::unique_ptr<Engine> e;
+};
+struct cs_transport {
+  std::unique_ptr<Transport> t;
+};
+struct cs_kvstore {
+  std::unique_ptr<KvStore> kv;
+  Engine* engine;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return CS_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CS_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return CS_ERR_INTERNAL;
+  }
+}
+
+std::vector<Tag> tags_of(const Engine& e, const uint64_t* ids, int n) {
+  if (n < 0 || (n > 0 && !ids)) throw UsageError("Engine: bad tag list");
+  std::vector<Tag> v;
+  v.reserve(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) v.push_back(e.tag_of(ids[i]));
+  return v;
+}
+
+OpKind kind_of(int k) {
+  switch (k) {
+    case CS_OP_COMPUTE: return OpKind::Compute;
+    case CS_OP_COPY: return OpKind::Copy;
+    case CS_OP_COLLECTIVE: return OpKind::Collective;
+    case CS_OP_OTHER: return OpKind::Other;
+  }
+  throw UsageError("Engine: unknown op kind");
+}
+
+TensorSlot slot_of(const Engine& e, const cs_slot& s) {
+  TensorSlot t;
+  t.data = s.data;
+  t.dtype = s.dtype;
+  t.numel = s.numel;
+  t.tag = e.tag_of(s.tag);
+  dtype_size(s.dtype);
+  if (s.numel > 0 && !s.data) throw UsageError("KvStore: null tensor data");
+  return t;
+}
+
+#define CHECK_HANDLE(h) \
+  if (!(h)) throw UsageError("null handle")
+}  // namespace
+
+extern "C" {
+
+const char* cs_last_error(void) { return g_last_error.c_str(); }
+
+const char* cs_status_name(int status) {
+  switch (status) {
+    case CS_OK: return "OK";
+    case CS_ERR_CONFIG: return "ConfigError";
+    case CS_ERR_USAGE: return "UsageError";
+    case CS_ERR_MISMATCH: return "MismatchError";
+    case CS_ERR_DEADLOCK: return "DeadlockTimeout";
+    case CS_ERR_ENGINE: return "EngineError";
+    case CS_ERR_CUDA: return "CudaError";
+    case CS_ERR_NCCL: return "NcclError";
+  }
+  return "InternalError";
+}
+
+int cs_version(void) { return 10000; }
+
+int cs_device_count(int* out) {
+  return guard([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+      cudaGetLastError();
+      n = 0;
+    } else if (e != cudaSuccess) {
+      throw_cuda(e, "cudaGetDeviceCount", __FILE__, __LINE__);
+    }
+    *out = n;
+  });
+}
+
+// ------------------------------------------------------------ kernels
+int cs_pack(const cs_copy_entry* entries, int n_entries, cs_dtype src_dt, cs_dtype dst_dt,
+            cs_stream_t stream) {
+  return guard([&] { pack(entries, n_entries, src_dt, dst_dt, reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+int cs_sum_buffers(const void* const* in, int m, void* const* out, int nout, uint64_t n,
+                   cs_dtype dt, cs_stream_t stream) {
+  return guard([&] { sum_buffers(in, m, out, nout, n, dt, reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+int cs_sgd_update(const cs_update_entry* entries, int n_entries, cs_dtype w_dt, cs_dtype g_dt,
+                  double lr, double rescale, double momentum, cs_stream_t stream) {
+  return guard([&] {
+    sgd_update(entries, n_entries, w_dt, g_dt, lr, rescale, momentum,
+               reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int cs_synth_backward(const void* src, void* dst, uint64_t n, cs_dtype dt, uint64_t spin_ns,
+                      int ctas, cs_stream_t stream) {
+  return guard([&] {
+    synth_backward(src, dst, n, dt, spin_ns, ctas, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int cs_checksum(const void* x, uint64_t n, cs_dtype dt, double* out_dev, cs_stream_t stream) {
+  return guard([&] { checksum(x, n, dt, out_dev, reinterpret_cast<cudaStream_t>(stream)); });
+}
+
+// -------------------------------------------------------------- trace
+int cs_trace_create(cs_trace_t* out) {
+  return guard([&] { *out = new cs_trace(); });
+}
+int cs_trace_destroy(cs_trace_t t) {
+  return guard([&] { delete t; });
+}
+int cs_trace_count(cs_trace_t t, uint64_t* out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *out = t->sink.count();
+  });
+}
+int cs_trace_write_jsonl(cs_trace_t t, const char* path) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->sink.write_jsonl(path);
+  });
+}
+int cs_trace_gauges(cs_trace_t t, int* max_open, int* overlap) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *max_open = t->sink.gauges().max_open_collectives.load();
+    *overlap = t->sink.gauges().compute_overlap.load() ? 1 : 0;
+  });
+}
+
+// ------------------------------------------------------------- engine
+int cs_engine_create(int num_worker_threads, int rank, int device, cs_trace_t trace,
+                     cs_engine_t* out) {
+  return guard([&] {
+    auto h = std::make_unique<cs_engine>();
+    h->e = std::make_unique<Engine>(num_worker_threads, rank, trace ? &trace->sink : nullptr, device);
+    *out = h.release();
+  });
+}
+int cs_engine_destroy(cs_engine_t e) {
+  return guard([&] { delete e; });
+}
+int cs_engine_new_variable(cs_engine_t e, uint64_t* tag) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    *tag = e->e->new_variable().id;
+  });
+}
+int cs_engine_push_host(cs_engine_t e, cs_host_fn fn, void* arg, const uint64_t* reads, int n_reads,
+                        const uint64_t* mutates, int n_mutates, int kind, int key, uint64_t* op_id) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    if (!fn) throw UsageError("Engine: null body");
+    OpId id = e->e->push([fn, arg] { if (fn(arg) != 0) throw EngineError("host op body failed"); }, tags_of(*e->e, reads, n_reads),
+                         tags_of(*e->e, mutates, n_mutates), kind_of(kind), key);
+    if (op_id) *op_id = id;
+  });
+}
+int cs_engine_push_stream(cs_engine_t e, cs_stream_fn fn, void* arg, const uint64_t* reads,
+                          int n_reads, const uint64_t* mutates, int n_mutates, int kind, int key,
+                          int lane, int dispatch, uint64_t* op_id) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    if (!fn) throw UsageError("Engine: null body");
+    if (dispatch != CS_DISPATCH_INLINE && dispatch != CS_DISPATCH_POOL)
+      throw UsageError("Engine: stream ops dispatch inline or on the pool");
+    OpId id = e->e->push_stream(
+        [fn, arg](cudaStream_t s) { if (fn(arg, reinterpret_cast<cs_stream_t>(s)) != 0) throw EngineError("stream op body failed"); },
+        tags_of(*e->e, reads, n_reads), tags_of(*e->e, mutates, n_mutates), kind_of(kind), key,
+        lane, dispatch == CS_DISPATCH_POOL ? Dispatch::Pool : Dispatch::Inline);
+    if (op_id) *op_id = id;
+  });
+}
+int cs_engine_wait_for(cs_engine_t e, uint64_t tag) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    e->e->wait_for(e->e->tag_of(tag));
+  });
+}
+int cs_engine_wait_all(cs_engine_t e) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    e->e->wait_all();
+  });
+}
+int cs_engine_shutdown(cs_engine_t e) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    e->e->shutdown();
+  });
+}
+int cs_engine_new_lane(cs_engine_t e, int priority, int* lane) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    *lane = e->e->new_lane(priority);
+  });
+}
+int cs_engine_lane_stream(cs_engine_t e, int lane, cs_stream_t* out) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    *out = reinterpret_cast<cs_stream_t>(e->e->lane_stream(lane));
+  });
+}
+int cs_engine_stats(cs_engine_t e, uint64_t* pushed, uint64_t* completed) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    *pushed = e->e->ops_pushed();
+    *completed = e->e->ops_completed();
+  });
+}
+int cs_engine_num_threads(cs_engine_t e, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    *out = e->e->num_threads();
+  });
+}
+
+// ---------------------------------------------------------- transport
+int cs_transport_create_local(int num_ranks, int watchdog_ms, cs_trace_t trace, cs_transport_t* out) {
+  return guard([&] {
+    auto h = std::make_unique<cs_transport>();
+    h->t = Transport::create_local(num_ranks, std::chrono::milliseconds(watchdog_ms),
+                                   trace ? &trace->sink : nullptr);
+    *out = h.release();
+  });
+}
+int cs_transport_create_nccl(const char* name, int num_ranks, int rank, int device, int watchdog_ms,
+                             cs_trace_t trace, cs_transport_t* out) {
+  return guard([&] {
+    auto h = std::make_unique<cs_transport>();
+    h->t = Transport::create_nccl(name ? name : "", num_ranks, rank, device,
+                                  std::chrono::milliseconds(watchdog_ms),
+                                  trace ? &trace->sink : nullptr);
+    *out = h.release();
+  });
+}
+int cs_transport_create_ledger_only(const char* name, int num_ranks, int rank, int watchdog_ms,
+                                    cs_trace_t trace, cs_transport_t* out) {
+  return guard([&] {
+    auto h = std::make_unique<cs_transport>();
+    h->t = Transport::create_ledger_only(name ? name : "", num_ranks, rank,
+                                         std::chrono::milliseconds(watchdog_ms),
+                                         trace ? &trace->sink : nullptr);
+    *out = h.release();
+  });
+}
+int cs_transport_destroy(cs_transport_t t) {
+  return guard([&] { delete t; });
+}
+int cs_transport_num_ranks(cs_transport_t t, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *out = t->t->num_ranks();
+  });
+}
+int cs_transport_num_communicators(cs_transport_t t, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *out = t->t->num_communicators();
+  });
+}
+int cs_transport_new_communicator(cs_transport_t t, int* comm) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *comm = t->t->new_communicator();
+  });
+}
+int cs_transport_set_inject_latency(cs_transport_t t, int64_t us) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->t->set_inject_latency(std::chrono::microseconds(us));
+  });
+}
+int cs_transport_abort(cs_transport_t t) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->t->abort("Transport: aborted by the caller");
+  });
+}
+int cs_allreduce_sum(cs_transport_t t, int comm, int rank, void* buf, uint64_t n, cs_dtype dt,
+                     int trace_key, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->t->allreduce_sum(comm, rank, buf, n, dt, trace_key, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int cs_broadcast(cs_transport_t t, int comm, int rank, int root, void* buf, uint64_t n, cs_dtype dt,
+                 int trace_key, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->t->broadcast(comm, rank, root, buf, n, dt, trace_key, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int cs_barrier(cs_transport_t t, int comm, int rank, int trace_key, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    t->t->barrier(comm, rank, trace_key, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+// ------------------------------------------------------------ kvstore
+int cs_create_communicators(cs_transport_t t, int count, int* comms_out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    std::vector<int> c = create_communicators(*t->t, count);
+    for (int i = 0; i < count; ++i) comms_out[i] = c[static_cast<size_t>(i)];
+  });
+}
+int cs_kv_create(cs_engine_t e, cs_transport_t t, int rank, const cs_kv_config* cfg,
+                 const int* concom_comms, int n_comms, cs_kvstore_t* out) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    CHECK_HANDLE(t);
+    CHECK_HANDLE(cfg);
+    KvConfig c;
+    if (cfg->mode < 0 || cfg->mode > 3) throw ConfigError("unknown kvstore mode");
+    c.mode = static_cast<KvMode>(cfg->mode);
+    c.outstanding = cfg->outstanding;
+    c.num_keys = cfg->num_keys;
+    c.comm_dtype = cfg->comm_dtype;
+    c.bucket_bytes = cfg->bucket_bytes;
+    c.issue_order = cfg->issue_order;
+    c.comm_priority = cfg->comm_priority;
+    std::vector<int> comms;
+    for (int i = 0; i < n_comms; ++i) comms.push_back(concom_comms[i]);
+    auto h = std::make_unique<cs_kvstore>();
+    h->engine = e->e.get();
+    h->kv = std::make_unique<KvStore>(*e->e, *t->t, rank, c, comms);
+    *out = h.release();
+  });
+}
+int cs_kv_destroy(cs_kvstore_t kv) {
+  return guard([&] { delete kv; });
+}
+int cs_kv_init(cs_kvstore_t kv, int key, cs_slot w) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    kv->kv->init(key, slot_of(*kv->engine, w));
+  });
+}
+int cs_kv_push(cs_kvstore_t kv, const int* keys, const cs_slot* grads, int n) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    std::vector<int> k(keys, keys + n);
+    std::vector<TensorSlot> s;
+    for (int i = 0; i < n; ++i) s.push_back(slot_of(*kv->engine, grads[i]));
+    kv->kv->push(k, s);
+  });
+}
+int cs_kv_pull(cs_kvstore_t kv, const int* keys, const cs_slot* outs, int n) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    std::vector<int> k(keys, keys + n);
+    std::vector<TensorSlot> s;
+    for (int i = 0; i < n; ++i) s.push_back(slot_of(*kv->engine, outs[i]));
+    kv->kv->pull(k, s);
+  });
+}
+int cs_kv_pull_update(cs_kvstore_t kv, const int* keys, const cs_slot* weights, int n,
+                      const cs_sgd* sgd) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    CHECK_HANDLE(sgd);
+    std::vector<int> k(keys, keys + n);
+    std::vector<TensorSlot> s;
+    for (int i = 0; i < n; ++i) s.push_back(slot_of(*kv->engine, weights[i]));
+    kv->kv->pull_update(k, s, SgdConfig{sgd->lr, sgd->rescale, sgd->momentum});
+  });
+}
+int cs_kv_barrier(cs_kvstore_t kv) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    kv->kv->barrier();
+  });
+}
+int cs_kv_outstanding_in_flight(cs_kvstore_t kv, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    *out = kv->kv->outstanding_in_flight();
+  });
+}
+int cs_kv_comm_buf(cs_kvstore_t kv, int key, void* host_out, uint64_t* numel, int* dtype) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    if (numel) *numel = kv->kv->key_numel(key);
+    if (dtype) *dtype = kv->kv->comm_dtype();
+    if (host_out) kv->kv->comm_buf(key, host_out);
+  });
+}
+int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    kv->kv->key_map(key, bucket, offset_elems);
+  });
+}
+int cs_kv_num_buckets(cs_kvstore_t kv, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    *out = kv->kv->num_buckets();
+  });
+}
+int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    *lane = kv->kv->bucket_lane(bucket);
+  });
+}
+
+}  // extern "C"

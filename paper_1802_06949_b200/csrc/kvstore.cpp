@@ -1,0 +1,436 @@
+// kvstore.cpp -- see kvstore.hpp.  Reference anchors (R/core/src/kvstore.cpp):
+//   construction / config checks   34-60
+//   init (rank-0 world broadcast)  76-97
+//   push (stage + per-mode comm)   99-143
+//   pull (copy-out / depcha op)    145-183
+//   barrier (drain + world)        185-193
+#include "kvstore.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.hpp"
+
+namespace csb {
+
+const char* kv_mode_name(KvMode m) {
+  switch (m) {
+    case KvMode::Funnel: return "funnel";
+    case KvMode::DepCha: return "depcha";
+    case KvMode::ConCom: return "concom";
+    case KvMode::Naive: return "naive";
+  }
+  return "unknown";
+}
+
+KvMode parse_kv_mode(const std::string& name) {
+  if (name == "funnel") return KvMode::Funnel;
+  if (name == "depcha") return KvMode::DepCha;
+  if (name == "concom") return KvMode::ConCom;
+  if (name == "naive") return KvMode::Naive;
+  throw ConfigError("unknown kvstore mode: " + name);
+}
+
+std::vector<int> create_communicators(Transport& transport, int count) {
+  std::vector<int> comms;
+  for (int i = 0; i < count; ++i) comms.push_back(transport.new_communicator());
+  return comms;
+}
+
+namespace {
+constexpr uint64_t kAlignBytes = 256;  // comm-slot alignment inside a fusion bucket
+
+void* device_alloc_zeroed(size_t bytes) {
+  void* p = nullptr;
+  CSB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  CSB_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 256)));
+  return p;
+}
+}  // namespace
+
+KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config,
+                 std::vector<int> concom_comms)
+    : engine_(engine),
+      transport_(transport),
+      rank_(rank),
+      cfg_(config),
+      comms_(std::move(concom_comms)) {
+  if (cfg_.num_keys < 1) throw ConfigError("KvStore: num_keys must be >= 1");
+  if (cfg_.mode == KvMode::ConCom) {
+    if (cfg_.outstanding < 1) throw ConfigError("KvStore: concom requires outstanding >= 1");
+    if (static_cast<int>(comms_.size()) != cfg_.outstanding)
+      throw ConfigError("KvStore: concom requires exactly `outstanding` communicators");
+  }
+  if (cfg_.comm_dtype >= 0) dtype_size(cfg_.comm_dtype);  // validates
+  comm_dt_ = cfg_.comm_dtype;
+  if (engine_.device() < 0) throw ConfigError("KvStore: the engine must be bound to a CUDA device");
+  keys_.resize(static_cast<size_t>(cfg_.num_keys));
+  init_order_tag_ = engine_.new_variable();
+  if (cfg_.mode == KvMode::DepCha) dummy_tag_ = engine_.new_variable();
+  if (cfg_.mode == KvMode::Funnel) funnel_tag_ = engine_.new_variable();
+  world_lane_ = engine_.new_lane(cfg_.comm_priority);
+  if (cfg_.mode == KvMode::ConCom)
+    for (int i = 0; i < cfg_.outstanding; ++i) comm_lanes_.push_back(engine_.new_lane(cfg_.comm_priority));
+}
+
+KvStore::~KvStore() {
+  try {
+    engine_.wait_all();
+  } catch (...) {
+  }
+  engine_.bind_device();
+  for (KeyState& k : keys_)
+    if (k.mom) cudaFree(k.mom);
+  for (void* p : allocations_) cudaFree(p);
+}
+
+void KvStore::check_key(int key, bool must_be_initialized) const {
+  if (key < 0 || key >= cfg_.num_keys) throw UsageError("KvStore: key out of range");
+  if (must_be_initialized && !keys_[static_cast<size_t>(key)].initialized)
+    throw UsageError("KvStore: key not initialized");
+}
+
+uint64_t KvStore::key_numel(int key) const {
+  check_key(key, true);
+  return keys_[static_cast<size_t>(key)].numel;
+}
+
+void KvStore::key_map(int key, int* bucket, uint64_t* offset) const {
+  check_key(key, true);
+  const KeyState& k = keys_[static_cast<size_t>(key)];
+  if (k.bucket < 0) throw UsageError("KvStore: fusion buckets are built at the first push");
+  *bucket = k.bucket;
+  *offset = k.offset;
+}
+
+int KvStore::bucket_lane(int b) const {
+  if (b < 0 || b >= num_buckets()) throw UsageError("KvStore: bucket out of range");
+  return buckets_[static_cast<size_t>(b)].lane;
+}
+
+void* KvStore::key_ptr(int key) const {
+  const KeyState& k = keys_[static_cast<size_t>(key)];
+  const Bucket& b = buckets_[static_cast<size_t>(k.bucket)];
+  return static_cast<char*>(b.base) + k.offset * dtype_size(comm_dt_);
+}
+
+void KvStore::init(int key, TensorSlot weights) {
+  check_key(key, false);
+  KeyState& ks = keys_[static_cast<size_t>(key)];
+  if (ks.initialized) throw UsageError("KvStore: duplicate init for key");
+  if (key != initialized_count_) throw UsageError("KvStore: keys must be initialized densely, in order");
+  if (weights.numel == 0) throw UsageError("Shape: extents must be >= 1");
+  if (comm_dt_ < 0) comm_dt_ = weights.dtype;
+  dtype_size(weights.dtype);
+  ks.numel = weights.numel;
+  ks.wdtype = weights.dtype;
+  ks.buf_tag = engine_.new_variable();
+  ks.initialized = true;
+  ++initialized_count_;
+
+  if (cfg_.bucket_bytes == 0) {
+    // reference map: comm_buf[key] 1:1 with the key (kvstore.cpp:84)
+    engine_.bind_device();
+    Bucket b;
+    b.keys = {key};
+    b.count = ks.numel;
+    b.base = device_alloc_zeroed(ks.numel * dtype_size(comm_dt_));
+    allocations_.push_back(b.base);
+    if (cfg_.mode == KvMode::ConCom) {
+      b.comm = comms_[static_cast<size_t>(key % cfg_.outstanding)];  // kvstore.cpp:119
+      b.lane = comm_lanes_[static_cast<size_t>(key % cfg_.outstanding)];
+    } else {
+      b.comm = Transport::world();
+      b.lane = world_lane_;
+    }
+    ks.bucket = static_cast<int>(buckets_.size());
+    ks.offset = 0;
+    buckets_.push_back(b);
+    built_ = (initialized_count_ == cfg_.num_keys);
+  }
+
+  // Rank 0's weights reach everyone through a world broadcast; the op
+  // mutates the weights plus a store-wide ordering tag so each rank issues
+  // its broadcasts in key order (kvstore.cpp:186-195).
+  Transport* tr = &transport_;
+  const int rank = rank_;
+  void* data = weights.data;
+  const uint64_t n = weights.numel;
+  const int dt = weights.dtype;
+  engine_.push_stream(
+      [tr, rank, data, n, dt, key](cudaStream_t s) {
+        tr->broadcast(Transport::world(), rank, 0, data, n, dt, key, s);
+      },
+      {}, {weights.tag, init_order_tag_}, OpKind::Collective, key, world_lane_, Dispatch::Pool);
+}
+
+// Fusion buckets: keys grouped greedily in issue order into buffers of at
+// most bucket_bytes (a larger key gets its own bucket); every key slot is
+// aligned to 256 B inside one zero-filled arena, so 16-byte vector access
+// holds for every key and the padding sums to zero.
+void KvStore::build_buckets() {
+  if (built_) return;
+  if (initialized_count_ != cfg_.num_keys)
+    throw UsageError("KvStore: fusion buckets need every key initialized before the first push");
+  const uint64_t es = dtype_size(comm_dt_);
+  const uint64_t align = kAlignBytes / es;
+  std::vector<int> order(static_cast<size_t>(cfg_.num_keys));
+  for (int k = 0; k < cfg_.num_keys; ++k)
+    order[static_cast<size_t>(k)] = cfg_.issue_order ? cfg_.num_keys - 1 - k : k;
+  std::vector<Bucket> bs;
+  Bucket cur;
+  uint64_t cur_bytes = 0;
+  for (int k : order) {
+    const uint64_t bytes = keys_[static_cast<size_t>(k)].numel * es;
+    if (!cur.keys.empty() && cur_bytes + bytes > cfg_.bucket_bytes) {
+      bs.push_back(cur);
+      cur = Bucket();
+      cur_bytes = 0;
+    }
+    KeyState& ks = keys_[static_cast<size_t>(k)];
+    ks.bucket = static_cast<int>(bs.size());
+    ks.offset = cur.count;
+    cur.keys.push_back(k);
+    cur.count = (cur.count + ks.numel + align - 1) / align * align;
+    cur_bytes += bytes;
+  }
+  if (!cur.keys.empty()) bs.push_back(cur);
+  uint64_t total = 0;
+  for (Bucket& b : bs) total += b.count;
+  engine_.bind_device();
+  char* arena = static_cast<char*>(device_alloc_zeroed(total * es));
+  allocations_.push_back(arena);
+  uint64_t off = 0;
+  for (size_t i = 0; i < bs.size(); ++i) {
+    Bucket& b = bs[i];
+    b.base = arena + off * es;
+    off += b.count;
+    if (cfg_.mode == KvMode::ConCom) {
+      b.comm = comms_[i % static_cast<size_t>(cfg_.outstanding)];
+      b.lane = comm_lanes_[i % static_cast<size_t>(cfg_.outstanding)];
+    } else {
+      b.comm = Transport::world();
+      b.lane = world_lane_;
+    }
+  }
+  buckets_ = std::move(bs);
+  built_ = true;
+}
+
+std::vector<std::pair<int, std::vector<int>>> KvStore::group_by_bucket(
+    const std::vector<int>& keys) const {
+  std::vector<std::pair<int, std::vector<int>>> groups;
+  for (size_t i = 0; i < keys.size(); ++i) {
+    const int b = keys_[static_cast<size_t>(keys[i])].bucket;
+    auto it = std::find_if(groups.begin(), groups.end(), [b](const auto& g) { return g.first == b; });
+    if (it == groups.end()) groups.push_back({b, {static_cast<int>(i)}});
+    else it->second.push_back(static_cast<int>(i));
+  }
+  return groups;
+}
+
+void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& grads) {
+  if (keys.size() != grads.size()) throw UsageError("KvStore: keys and values differ in length");
+  for (size_t i = 0; i < keys.size(); ++i) {
+    check_key(keys[i], true);
+    const KeyState& ks = keys_[static_cast<size_t>(keys[i])];
+    if (grads[i].numel != ks.numel)
+      throw UsageError("KvStore: pushed gradient shape differs from init shape");
+    if (ks.pushed) throw UsageError("KvStore: key pushed twice without a pull");
+    for (size_t j = 0; j < i; ++j)
+      if (keys[j] == keys[i]) throw UsageError("KvStore: duplicate key in one push");
+  }
+  build_buckets();
+
+  for (const auto& [b, idxs] : group_by_bucket(keys)) {
+    Bucket& B = buckets_[static_cast<size_t>(b)];
+    // stage every gradient of this call into its bucket slot: kernel (a),
+    // one launch per bucket (kvstore.cpp:109 `copy(g, comm_buf)`)
+    std::vector<cs_copy_entry> entries;
+    std::vector<Tag> reads, muts;
+    int src_dt = -1;
+    for (int i : idxs) {
+      const int k = keys[static_cast<size_t>(i)];
+      const TensorSlot& g = grads[static_cast<size_t>(i)];
+      if (src_dt < 0) src_dt = g.dtype;
+      if (g.dtype != src_dt) throw UsageError("KvStore: one push mixes gradient dtypes in a bucket");
+      entries.push_back(cs_copy_entry{g.data, key_ptr(k), g.numel});
+      reads.push_back(g.tag);
+      muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
+      keys_[static_cast<size_t>(k)].pushed = true;
+    }
+    const int dst_dt = comm_dt_;
+    const int key0 = keys[static_cast<size_t>(idxs[0])];
+    engine_.push_stream(
+        [entries, src_dt, dst_dt](cudaStream_t s) {
+          pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
+        },
+        reads, muts, OpKind::Copy, key0, B.lane, Dispatch::Inline);
+    B.pushed += static_cast<int>(idxs.size());
+
+    if (B.pushed == static_cast<int>(B.keys.size()) &&
+        (cfg_.mode == KvMode::Funnel || cfg_.mode == KvMode::ConCom))
+      issue_collective(b, reads);
+  }
+}
+
+void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
+  Bucket& B = buckets_[static_cast<size_t>(b)];
+  std::vector<Tag> muts;
+  for (int k : B.keys) muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
+  Transport* tr = &transport_;
+  const int rank = rank_;
+  const int key0 = B.keys[0];
+  const int bid = cfg_.bucket_bytes ? b : -1;
+  void* base = B.base;
+  const uint64_t count = B.count;
+  const int comm = B.comm;
+  const int dt = comm_dt_;
+  B.issued = true;
+  if (cfg_.mode == KvMode::Funnel) {
+    // control-thread collective on the single ordered comm stream
+    // (kvstore.cpp:112-116); the funnel tag keeps issue order = push order
+    muts.push_back(funnel_tag_);
+    engine_.push_stream(
+        [tr, rank, base, count, dt, key0, bid](cudaStream_t s) {
+          tr->allreduce_sum(Transport::world(), rank, base, count, dt, key0, s, bid);
+        },
+        {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+  } else {
+    // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136)
+    std::atomic<int>* outstanding = &outstanding_;
+    outstanding_.fetch_add(1);
+    std::vector<Tag> reads = extra_reads;
+    engine_.push_stream(
+        [tr, outstanding, comm, rank, base, count, dt, key0, bid](cudaStream_t s) {
+          struct Drain {
+            std::atomic<int>* c;
+            ~Drain() {
+              c->fetch_sub(1);
+              c->notify_all();
+            }
+          } drain{outstanding};
+          tr->allreduce_sum(comm, rank, base, count, dt, key0, s, bid);
+        },
+        reads, muts, OpKind::Collective, key0, B.lane, Dispatch::Pool);
+  }
+}
+
+void KvStore::pull(const std::vector<int>& keys, const std::vector<TensorSlot>& outs) {
+  pull_impl(keys, outs, nullptr);
+}
+
+void KvStore::pull_update(const std::vector<int>& keys, const std::vector<TensorSlot>& weights,
+                          const SgdConfig& sgd) {
+  pull_impl(keys, weights, &sgd);
+}
+
+void KvStore::ensure_momentum(int key, int wdt) {
+  KeyState& ks = keys_[static_cast<size_t>(key)];
+  if (ks.mom) return;
+  engine_.bind_device();
+  const size_t es = (wdt == CS_F64) ? 8 : 4;
+  CSB_CUDA(cudaMalloc(&ks.mom, std::max<size_t>(ks.numel * es, 256)));
+  CSB_CUDA(cudaMemset(ks.mom, 0, std::max<size_t>(ks.numel * es, 256)));
+  CSB_CUDA(cudaDeviceSynchronize());  // one-time: zeroed before any lane touches it
+}
+
+void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSlot>& outs,
+                        const SgdConfig* sgd) {
+  if (keys.size() != outs.size()) throw UsageError("KvStore: keys and values differ in length");
+  for (size_t i = 0; i < keys.size(); ++i) {
+    check_key(keys[i], true);
+    const KeyState& ks = keys_[static_cast<size_t>(keys[i])];
+    if (!ks.pushed) throw UsageError("KvStore: pull without a preceding push this iteration");
+    if (outs[i].numel != ks.numel) throw UsageError("KvStore: pull output shape differs from init shape");
+    for (size_t j = 0; j < i; ++j)
+      if (keys[j] == keys[i]) throw UsageError("KvStore: duplicate key in one pull");
+  }
+  const bool momentum = sgd && sgd->momentum != 0.0;
+
+  for (const auto& [b, idxs] : group_by_bucket(keys)) {
+    Bucket& B = buckets_[static_cast<size_t>(b)];
+    if (B.pushed != static_cast<int>(B.keys.size()))
+      throw UsageError("KvStore: pull of a fusion bucket before all of its keys were pushed");
+    std::vector<Tag> buf_tags, out_tags;
+    std::vector<cs_copy_entry> copies;
+    std::vector<cs_update_entry> updates;
+    int out_dt = -1;
+    for (int i : idxs) {
+      const int k = keys[static_cast<size_t>(i)];
+      const TensorSlot& o = outs[static_cast<size_t>(i)];
+      if (out_dt < 0) out_dt = o.dtype;
+      if (o.dtype != out_dt) throw UsageError("KvStore: one pull mixes output dtypes in a bucket");
+      buf_tags.push_back(keys_[static_cast<size_t>(k)].buf_tag);
+      out_tags.push_back(o.tag);
+      if (sgd) {
+        if (momentum) ensure_momentum(k, o.dtype);
+        updates.push_back(cs_update_entry{o.data, key_ptr(k), keys_[static_cast<size_t>(k)].mom, o.numel});
+      } else {
+        copies.push_back(cs_copy_entry{key_ptr(k), o.data, o.numel});
+      }
+    }
+    const int cdt = comm_dt_;
+    const SgdConfig opt = sgd ? *sgd : SgdConfig{};
+    const bool upd = sgd != nullptr;
+    // unpack (kvstore.cpp:160/170 copy) or the fused SGD update, kernel (a)/(c)
+    auto finish = [copies, updates, cdt, out_dt, opt, upd](cudaStream_t s) {
+      if (upd) sgd_update(updates.data(), static_cast<int>(updates.size()), out_dt, cdt, opt.lr,
+                          opt.rescale, opt.momentum, s);
+      else pack(copies.data(), static_cast<int>(copies.size()), cdt, out_dt, s);
+    };
+    const int key0 = keys[static_cast<size_t>(idxs[0])];
+
+    if ((cfg_.mode == KvMode::DepCha || cfg_.mode == KvMode::Naive) && !B.issued) {
+      // one op {allreduce; copy-out} (kvstore.cpp:163-179).  The allreduce
+      // rewrites the comm buffer, so it is modelled as a write (the
+      // reference holds only a read grant there).
+      std::vector<Tag> muts;
+      for (int k : B.keys) muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
+      for (const Tag& t : out_tags) muts.push_back(t);
+      if (cfg_.mode == KvMode::DepCha) muts.push_back(dummy_tag_);
+      Transport* tr = &transport_;
+      const int rank = rank_;
+      void* base = B.base;
+      const uint64_t count = B.count;
+      const int ckey = B.keys[0];
+      const int bid = cfg_.bucket_bytes ? b : -1;
+      B.issued = true;
+      engine_.push_stream(
+          [tr, rank, base, count, cdt, ckey, bid, finish](cudaStream_t s) {
+            tr->allreduce_sum(Transport::world(), rank, base, count, cdt, ckey, s, bid);
+            finish(s);
+          },
+          {}, muts, OpKind::Collective, ckey, B.lane, Dispatch::Pool);
+    } else {
+      engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
+                          B.lane, Dispatch::Inline);
+    }
+    for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;
+    B.pulled += static_cast<int>(idxs.size());
+    if (B.pulled == static_cast<int>(B.keys.size())) {
+      B.pushed = 0;
+      B.pulled = 0;
+      B.issued = false;
+    }
+  }
+}
+
+// kvstore.cpp:185-193: drain the in-flight counter, then a world barrier.
+void KvStore::barrier() {
+  if (cfg_.mode != KvMode::ConCom) return;
+  for (int v = outstanding_.load(); v != 0; v = outstanding_.load()) outstanding_.wait(v);
+  engine_.bind_device();
+  transport_.barrier(Transport::world(), rank_, -1, engine_.lane_stream(world_lane_));
+}
+
+void KvStore::comm_buf(int key, void* host_out) {
+  check_key(key, true);
+  const KeyState& ks = keys_[static_cast<size_t>(key)];
+  if (ks.bucket < 0) throw UsageError("KvStore: comm buffer not allocated yet");
+  engine_.wait_for(ks.buf_tag);
+  engine_.bind_device();
+  CSB_CUDA(cudaMemcpy(host_out, key_ptr(key), ks.numel * dtype_size(comm_dt_), cudaMemcpyDeviceToHost));
+}
+
+}  // namespace csb

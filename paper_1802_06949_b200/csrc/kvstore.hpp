@@ -1,0 +1,141 @@
+// kvstore.hpp -- per-rank init/push/pull/barrier facade (reference:
+// R/core/include/collsim/kvstore.hpp:13-96, R/core/src/kvstore.cpp).
+//
+// Schedules (kvstore.hpp:39-53 of the reference), B200 treatment:
+//   funnel  push stages the gradient and issues the allreduce from the
+//           control thread onto ONE ordered comm stream; collectives carry
+//           a funnel ordering tag so they are issued in push order.
+//   depcha  push only stages; pull issues one op {allreduce; unpack/update}
+//           that also mutates the shared dummy tag, so the engine's in-order
+//           write rule chains the collectives: every rank issues them in
+//           the same order, and the GPU sees a cudaStreamWaitEvent chain.
+//   concom  push stages, then hands the allreduce to the pool on
+//           comms[bucket % outstanding], one NCCL communicator and one
+//           CUDA stream each; barrier() drains the in-flight counter and
+//           runs a world barrier.
+//   naive   depcha without the dummy tag (deliberately broken; the ledger
+//           turns the misordering into MismatchError / DeadlockTimeout).
+// Extensions: comm buffers in any dtype (fp32 grads -> bf16 buckets),
+// fusion buckets (keys grouped in issue order, one collective per bucket),
+// list push/pull (MXNet KVStore key lists), and pull fused with the SGD /
+// momentum update (kernel (c) reads the reduced bucket, the copy-back of
+// kvstore.cpp:160/170 disappears).
+#pragma once
+
+#include <atomic>
+#include <vector>
+
+#include "engine.hpp"
+#include "transport.hpp"
+
+namespace csb {
+
+enum class KvMode { Funnel = 0, DepCha = 1, ConCom = 2, Naive = 3 };
+const char* kv_mode_name(KvMode m);
+KvMode parse_kv_mode(const std::string& name);
+
+struct KvConfig {
+  KvMode mode = KvMode::Funnel;
+  int outstanding = 1;
+  int num_keys = 0;
+  int comm_dtype = -1;        // -1: dtype of the init weights
+  uint64_t bucket_bytes = 0;  // 0: one buffer per key (reference map)
+  int issue_order = 0;        // bucket grouping order: 0 ascending, 1 descending
+  int comm_priority = 0;      // CUDA stream priority of the comm lanes
+};
+
+// Non-owning device view + engine tag (kvstore.hpp:16-19).
+struct TensorSlot {
+  void* data = nullptr;
+  int dtype = CS_F32;
+  uint64_t numel = 0;
+  Tag tag;
+};
+
+struct SgdConfig {
+  double lr = 0.1;
+  double rescale = 1.0;
+  double momentum = 0.0;
+};
+
+std::vector<int> create_communicators(Transport& transport, int count);
+
+class KvStore {
+ public:
+  KvStore(Engine& engine, Transport& transport, int rank, KvConfig config,
+          std::vector<int> concom_comms = {});
+  ~KvStore();
+  KvStore(const KvStore&) = delete;
+  KvStore& operator=(const KvStore&) = delete;
+
+  void init(int key, TensorSlot weights);
+  void push(int key, TensorSlot grad) { push(std::vector<int>{key}, std::vector<TensorSlot>{grad}); }
+  void pull(int key, TensorSlot out) { pull(std::vector<int>{key}, std::vector<TensorSlot>{out}); }
+  void push(const std::vector<int>& keys, const std::vector<TensorSlot>& grads);
+  void pull(const std::vector<int>& keys, const std::vector<TensorSlot>& outs);
+  void pull_update(const std::vector<int>& keys, const std::vector<TensorSlot>& weights,
+                   const SgdConfig& sgd);
+  void barrier();
+
+  int rank() const { return rank_; }
+  const KvConfig& config() const { return cfg_; }
+  int outstanding_in_flight() const { return outstanding_.load(); }
+  // Synchronizes the key's comm buffer and copies it to host memory.
+  void comm_buf(int key, void* host_out);
+  int comm_dtype() const { return comm_dt_; }
+  uint64_t key_numel(int key) const;
+  void key_map(int key, int* bucket, uint64_t* offset) const;
+  int num_buckets() const { return static_cast<int>(buckets_.size()); }
+  int bucket_lane(int b) const;
+
+ private:
+  struct KeyState {
+    uint64_t numel = 0;
+    int wdtype = -1;
+    bool initialized = false;
+    bool pushed = false;
+    int bucket = -1;
+    uint64_t offset = 0;  // elements into the bucket buffer
+    Tag buf_tag;
+    void* mom = nullptr;  // momentum state (lazy)
+  };
+  struct Bucket {
+    std::vector<int> keys;  // in bucket order
+    uint64_t count = 0;     // elements in the collective (incl. alignment padding)
+    void* base = nullptr;
+    int pushed = 0;
+    int pulled = 0;
+    bool issued = false;  // collective issued this iteration
+    int comm = 0;
+    int lane = 0;
+  };
+
+  void check_key(int key, bool must_be_initialized) const;
+  void build_buckets();
+  std::vector<std::pair<int, std::vector<int>>> group_by_bucket(const std::vector<int>& keys) const;
+  void issue_collective(int b, const std::vector<Tag>& extra_reads);
+  void pull_impl(const std::vector<int>& keys, const std::vector<TensorSlot>& outs,
+                 const SgdConfig* sgd);
+  void* key_ptr(int key) const;
+  void ensure_momentum(int key, int wdt);
+
+  Engine& engine_;
+  Transport& transport_;
+  const int rank_;
+  const KvConfig cfg_;
+  std::vector<int> comms_;
+  int comm_dt_ = -1;
+  std::vector<KeyState> keys_;
+  std::vector<Bucket> buckets_;
+  std::vector<void*> allocations_;
+  int world_lane_ = 0;
+  std::vector<int> comm_lanes_;  // concom: lane per extra communicator
+  Tag init_order_tag_;
+  Tag dummy_tag_;
+  Tag funnel_tag_;
+  int initialized_count_ = 0;
+  bool built_ = false;
+  std::atomic<int> outstanding_{0};
+};
+
+}  // namespace csb

@@ -1,0 +1,281 @@
+// transport.cpp -- see transport.hpp.
+#include "transport.hpp"
+
+#include "kernels.hpp"
+
+namespace csb {
+
+namespace {
+
+[[noreturn]] void throw_nccl(ncclResult_t r, const char* what, ncclComm_t comm) {
+  std::string msg = std::string(what) + ": " + ncclGetErrorString(r);
+  const char* last = ncclGetLastError(comm);
+  if (last && last[0]) msg += std::string(" (") + last + ")";
+  throw NcclError(msg);
+}
+
+#define CSB_NCCL(call, comm)                                \
+  do {                                                      \
+    ncclResult_t csb_r_ = (call);                           \
+    if (csb_r_ != ncclSuccess) throw_nccl(csb_r_, #call, comm); \
+  } while (0)
+
+ncclDataType_t nccl_type(int dt) {
+  switch (dt) {
+    case CS_F64: return ncclFloat64;
+    case CS_F32: return ncclFloat32;
+    case CS_BF16: return ncclBfloat16;
+  }
+  throw UsageError("collective: unknown dtype");
+}
+
+int current_device() {
+  int d = 0;
+  CSB_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+// (Re)creates `ev` on the calling thread's device when needed.
+void ensure_event(cudaEvent_t& ev, int& ev_dev) {
+  const int d = current_device();
+  if (ev && ev_dev == d) return;
+  if (ev) {
+    int prev = d;
+    cudaSetDevice(ev_dev);
+    cudaEventDestroy(ev);
+    cudaSetDevice(prev);
+  }
+  CSB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  ev_dev = d;
+}
+
+}  // namespace
+
+struct Transport::SlotDev {
+  void* bufs[kLedgerMaxRanks] = {};
+  cudaEvent_t ready[kLedgerMaxRanks] = {};
+  int ready_dev[kLedgerMaxRanks] = {};
+  cudaEvent_t done = nullptr;
+  int done_dev = -1;
+  ~SlotDev() {
+    for (int r = 0; r < kLedgerMaxRanks; ++r)
+      if (ready[r]) {
+        cudaSetDevice(ready_dev[r]);
+        cudaEventDestroy(ready[r]);
+      }
+    if (done) {
+      cudaSetDevice(done_dev);
+      cudaEventDestroy(done);
+    }
+  }
+};
+
+std::unique_ptr<Transport> Transport::create_local(int nranks, std::chrono::milliseconds watchdog,
+                                                   TraceSink* trace) {
+  std::unique_ptr<Transport> t(new Transport());
+  t->backend_ = Backend::Local;
+  t->ledger_ = Ledger::create_local(nranks, watchdog, trace);
+  t->slots_.resize(static_cast<size_t>(kLedgerMaxComms) * kLedgerSlots);
+  return t;
+}
+
+std::unique_ptr<Transport> Transport::create_ledger_only(const std::string& name, int nranks,
+                                                         int rank,
+                                                         std::chrono::milliseconds watchdog,
+                                                         TraceSink* trace) {
+  std::unique_ptr<Transport> t(new Transport());
+  t->backend_ = Backend::LedgerOnly;
+  if (name.empty()) {
+    t->ledger_ = Ledger::create_local(nranks, watchdog, trace);
+  } else {
+    t->ledger_ = Ledger::create_shm(name, nranks, rank, watchdog, trace);
+    t->rank_ = rank;
+  }
+  return t;
+}
+
+std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int nranks, int rank,
+                                                  int device, std::chrono::milliseconds watchdog,
+                                                  TraceSink* trace) {
+  std::unique_ptr<Transport> t(new Transport());
+  t->backend_ = Backend::Nccl;
+  t->rank_ = rank;
+  t->device_ = device;
+  t->ledger_ = Ledger::create_shm(name, nranks, rank, watchdog, trace);
+  CSB_CUDA(cudaSetDevice(device));
+  ncclUniqueId id;
+  if (rank == 0) {
+    CSB_NCCL(ncclGetUniqueId(&id), nullptr);
+    t->ledger_->post_blob(0, &id, sizeof(id));
+  } else {
+    t->ledger_->read_blob(0, &id, sizeof(id));
+  }
+  ncclComm_t world = nullptr;
+  CSB_NCCL(ncclCommInitRank(&world, nranks, id, rank), nullptr);
+  t->comms_.push_back(world);
+  return t;
+}
+
+Transport::~Transport() {
+  if (backend_ == Backend::Nccl) {
+    const bool aborted = ledger_ && ledger_->latched();
+    cudaSetDevice(device_);
+    for (ncclComm_t c : comms_) {
+      if (!c) continue;
+      if (aborted) ncclCommAbort(c);
+      else ncclCommDestroy(c);
+    }
+  }
+}
+
+int Transport::new_communicator() {
+  const int id = ledger_->new_communicator();
+  if (backend_ == Backend::Nccl) {
+    std::lock_guard<std::mutex> lock(mu_);
+    CSB_CUDA(cudaSetDevice(device_));
+    ncclComm_t c = nullptr;
+    CSB_NCCL(ncclCommSplit(comms_[0], 0, rank_, &c, nullptr), comms_[0]);
+    if (static_cast<int>(comms_.size()) != id) throw UsageError("Transport: communicator ids diverged");
+    comms_.push_back(c);
+  }
+  return id;
+}
+
+void Transport::set_inject_latency(std::chrono::microseconds us) { ledger_->set_inject_latency(us); }
+
+void Transport::abort(const std::string& why) {
+  ledger_->abort(why);
+  if (backend_ == Backend::Nccl) {
+    std::lock_guard<std::mutex> lock(mu_);
+    for (ncclComm_t& c : comms_) {
+      if (c) ncclCommAbort(c);
+      c = nullptr;
+    }
+  }
+}
+
+void Transport::allreduce_sum(int comm, int rank, void* buf, uint64_t count, int dtype,
+                              int trace_key, cudaStream_t stream, int bucket) {
+  if (count == 0) throw UsageError("allreduce_sum: empty buffer");  // collective.cpp:63-69
+  CallSig sig;
+  sig.kind = CollKind::AllreduceSum;
+  sig.dtype = dtype;
+  sig.count = static_cast<int64_t>(count);
+  run(comm, rank, sig, buf, trace_key, stream, bucket);
+}
+
+void Transport::broadcast(int comm, int rank, int root, void* buf, uint64_t count, int dtype,
+                          int trace_key, cudaStream_t stream) {
+  if (root < 0 || root >= num_ranks()) throw UsageError("broadcast: root out of range");
+  CallSig sig;
+  sig.kind = CollKind::Broadcast;
+  sig.dtype = dtype;
+  sig.count = static_cast<int64_t>(count);
+  sig.root = root;
+  run(comm, rank, sig, buf, trace_key, stream, -1);
+}
+
+void Transport::barrier(int comm, int rank, int trace_key, cudaStream_t stream) {
+  CallSig sig;
+  sig.kind = CollKind::Barrier;
+  run(comm, rank, sig, nullptr, trace_key, stream, -1);
+}
+
+void Transport::device_latency(cudaStream_t stream) {
+  const auto lat = ledger_->inject_latency();
+  if (lat.count() > 0 && stream)
+    synth_backward(nullptr, nullptr, 0, CS_F32, static_cast<uint64_t>(lat.count()) * 1000, 1, stream);
+}
+
+void Transport::run(int comm, int rank, const CallSig& sig, void* buf, int trace_key,
+                    cudaStream_t stream, int bucket) {
+  if (backend_ != Backend::LedgerOnly && sig.kind != CollKind::Barrier && sig.count > 0 && !buf)
+    throw UsageError("collective: null buffer");
+  std::function<void(const Ledger::Ticket&)> publish;
+  if (backend_ == Backend::Local && sig.kind != CollKind::Barrier) {
+    publish = [&](const Ledger::Ticket& t) {
+      SlotDev* sd;
+      {
+        std::lock_guard<std::mutex> lock(mu_);
+        auto& p = slots_[ledger_->slot_uid(t)];
+        if (!p) p = std::make_unique<SlotDev>();
+        sd = p.get();
+      }
+      sd->bufs[rank] = buf;
+      ensure_event(sd->ready[rank], sd->ready_dev[rank]);
+      CSB_CUDA(cudaEventRecord(sd->ready[rank], stream));
+    };
+  }
+  Ledger::Ticket t = ledger_->arrive(comm, rank, sig, trace_key, bucket, publish);
+  if (t.last) {
+    try {
+      if (backend_ == Backend::Local && sig.kind != CollKind::Barrier) local_data(t, sig, buf, stream);
+    } catch (...) {
+      ledger_->abort("collective: reducer failed to enqueue");
+      ledger_->finish(t);
+      throw;
+    }
+    ledger_->finish(t);
+  } else if (backend_ == Backend::Local && sig.kind != CollKind::Barrier && sig.count > 0) {
+    SlotDev* sd;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      sd = slots_[ledger_->slot_uid(t)].get();
+    }
+    CSB_CUDA(cudaStreamWaitEvent(stream, sd->done, 0));
+  }
+  if (backend_ == Backend::Nccl && sig.kind != CollKind::Barrier && sig.count > 0) {
+    device_latency(stream);
+    nccl_data(comm, sig, buf, stream);
+  }
+  ledger_->depart(t, trace_key, bucket);
+}
+
+// Last arriver of an in-process rendezvous: fixed rank-order reduction of
+// every rank's buffer by kernel (b), result written to all of them
+// (collective.cpp:228-236), or root -> everyone copy (collective.cpp:237-243).
+void Transport::local_data(const Ledger::Ticket& t, const CallSig& sig, void* buf,
+                           cudaStream_t stream) {
+  SlotDev* sd;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    sd = slots_[ledger_->slot_uid(t)].get();
+  }
+  const int R = num_ranks();
+  for (int r = 0; r < R; ++r)
+    if (r != t.rank) CSB_CUDA(cudaStreamWaitEvent(stream, sd->ready[r], 0));
+  if (sig.count > 0) {
+    device_latency(stream);
+    if (sig.kind == CollKind::AllreduceSum) {
+      if (R > 1) sum_buffers(sd->bufs, R, sd->bufs, R, static_cast<uint64_t>(sig.count), sig.dtype, stream);
+    } else {
+      const void* src[1] = {sd->bufs[sig.root]};
+      void* dst[kLedgerMaxRanks];
+      int nd = 0;
+      for (int r = 0; r < R; ++r)
+        if (r != sig.root) dst[nd++] = sd->bufs[r];
+      if (nd > 0) sum_buffers(src, 1, dst, nd, static_cast<uint64_t>(sig.count), sig.dtype, stream);
+    }
+  }
+  (void)buf;
+  ensure_event(sd->done, sd->done_dev);
+  CSB_CUDA(cudaEventRecord(sd->done, stream));
+}
+
+void Transport::nccl_data(int comm, const CallSig& sig, void* buf, cudaStream_t stream) {
+  ncclComm_t c;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (comm < 0 || comm >= static_cast<int>(comms_.size()) || !comms_[comm])
+      throw UsageError("collective: communicator not available");
+    c = comms_[comm];
+  }
+  const ncclDataType_t ty = nccl_type(sig.dtype);
+  if (sig.kind == CollKind::AllreduceSum) {
+    CSB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(sig.count), ty, ncclSum, c, stream), c);
+  } else if (sig.kind == CollKind::Broadcast) {
+    CSB_NCCL(ncclBroadcast(buf, buf, static_cast<size_t>(sig.count), ty, sig.root, c, stream), c);
+  }
+}
+
+}  // namespace csb

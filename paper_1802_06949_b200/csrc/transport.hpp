@@ -1,0 +1,85 @@
+// transport.hpp -- collectives over device memory.
+//
+// Reference interface: R/core/include/collsim/collective.hpp:36-61
+// (Transport{num_ranks, world, new_communicator, allreduce_sum, broadcast,
+// barrier, set_inject_latency}).  Every call first goes through the matching
+// Ledger (issue order, signature, watchdog, latch); only a matched call
+// touches the device, stream-ordered on the caller's stream:
+//
+//   Backend::Local  in-process rank threads (one GPU or several, UVA peers).
+//                   The last arriver waits on every rank's ready event and
+//                   runs kernel (b) over all R buffers in fixed rank order,
+//                   writing the sum to every buffer -- the reference's
+//                   "last arriver reduces" (collective.cpp:228-243) on HBM,
+//                   bit-identical to it.  The others make their stream wait
+//                   on the reducer's done event.
+//   Backend::Nccl   one process per GPU; ledger in POSIX shm; data over NCCL
+//                   (NVLink 5 / NVSwitch).  One ncclComm_t per communicator
+//                   (world + ConCom's extra communicators, ncclCommSplit).
+//   Backend::LedgerOnly  matching only (CPU tests of the host logic).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ledger.hpp"
+
+namespace csb {
+
+class Transport {
+ public:
+  enum class Backend { Local, Nccl, LedgerOnly };
+
+  static std::unique_ptr<Transport> create_local(int nranks, std::chrono::milliseconds watchdog,
+                                                 TraceSink* trace);
+  static std::unique_ptr<Transport> create_nccl(const std::string& name, int nranks, int rank,
+                                                int device, std::chrono::milliseconds watchdog,
+                                                TraceSink* trace);
+  static std::unique_ptr<Transport> create_ledger_only(const std::string& name, int nranks,
+                                                       int rank, std::chrono::milliseconds watchdog,
+                                                       TraceSink* trace);
+  ~Transport();
+
+  int num_ranks() const { return ledger_->num_ranks(); }
+  static constexpr int world() { return 0; }
+  Backend backend() const { return backend_; }
+  int local_rank() const { return rank_; }
+
+  int new_communicator();
+  int num_communicators() const { return ledger_->num_communicators(); }
+
+  void allreduce_sum(int comm, int rank, void* buf, uint64_t count, int dtype, int trace_key,
+                     cudaStream_t stream, int bucket = -1);
+  void broadcast(int comm, int rank, int root, void* buf, uint64_t count, int dtype,
+                 int trace_key, cudaStream_t stream);
+  void barrier(int comm, int rank, int trace_key, cudaStream_t stream);
+
+  void set_inject_latency(std::chrono::microseconds us);
+  void abort(const std::string& why);
+  Ledger& ledger() { return *ledger_; }
+
+ private:
+  Transport() = default;
+  struct SlotDev;  // per (comm, ring slot) payload of the local backend
+  void run(int comm, int rank, const CallSig& sig, void* buf, int trace_key, cudaStream_t stream,
+           int bucket);
+  void local_data(const Ledger::Ticket& t, const CallSig& sig, void* buf, cudaStream_t stream);
+  void nccl_data(int comm, const CallSig& sig, void* buf, cudaStream_t stream);
+  void device_latency(cudaStream_t stream);
+
+  Backend backend_ = Backend::LedgerOnly;
+  int rank_ = -1;
+  int device_ = -1;
+  std::unique_ptr<Ledger> ledger_;
+  std::vector<ncclComm_t> comms_;  // nccl: index = communicator id
+  std::vector<std::unique_ptr<SlotDev>> slots_;  // local: comm * kLedgerSlots + slot
+  std::mutex mu_;
+};
+
+}  // namespace csb

@@ -1,0 +1,610 @@
+"""KvStore schedules on the GPU (in-process rank threads over the local
+transport: kernel (b) reduces in rank order on HBM).  Ports of the reference's
+test_kvstore.cpp / acceptance.cpp cases plus parity against golden fixtures
+frozen from the reference itself (tests/golden/make_golden.py)."""
+import json
+import threading
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from kvhelpers import kv_ranks
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_1802_06949_b200 import (KvConfig, MismatchError, DeadlockTimeout, Slot,  # noqa: E402
+                                   TraceSink, Transport, UsageError, api)
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def t64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def slot(eng, value):
+    return Slot(value, eng.new_variable())
+
+
+def producer(eng, src, dst_slot, key):
+    """Synthetic backward op: dst <- src on the compute lane (mutates dst tag)."""
+    n, dt = dst_slot.value.numel(), api.dtype_code(dst_slot.value.dtype)
+    s, d = src.data_ptr(), dst_slot.value.data_ptr()
+    eng.push_stream(lambda st: api.synth_backward(s, d, n, dt, 0, 0, st), [], [dst_slot.tag],
+                    api.COMPUTE, key)
+
+
+def sgd_op(eng, w, g, lr, rescale, key):
+    """push_sgd_update (trainer.cpp:74-80) as a stream op running kernel (c)."""
+    n = w.value.numel()
+    wp, gp = w.value.data_ptr(), g.value.data_ptr()
+    eng.push_stream(lambda st: api.sgd_update([(wp, gp, 0, n)], api.F64, api.F64, lr, rescale, 0.0, st),
+                    [g.tag], [w.tag], api.COMPUTE, key)
+
+
+def enqueued(events, rank=None):
+    return [e for e in events if e["event"] == "coll_enqueued" and (rank is None or e["rank"] == rank)]
+
+
+# ----------------------------------------------------------- reference ports
+
+def test_init_broadcasts_rank0_weights(gpu):
+    transport = Transport.local(2, 5000)
+    init = O.random_uniform(6, 5)
+    results = [None, None]
+
+    def body(rank, eng, store):
+        w = slot(eng, t64(init if rank == 0 else np.zeros(6)))
+        store.init(0, w)
+        eng.wait_all()
+        results[rank] = w.value.cpu().numpy()
+
+    kv_ranks(2, 2, KvConfig("funnel", 1, 1), transport, None, body)
+    np.testing.assert_array_equal(results[0], init)
+    np.testing.assert_array_equal(results[1], init)
+
+
+def test_init_validates_keys(gpu):
+    transport = Transport.local(1, 5000)
+
+    def body(rank, eng, store):
+        w = slot(eng, t64(np.ones(2)))
+        with pytest.raises(UsageError):
+            store.init(1, w)  # out of order
+        store.init(0, w)
+        with pytest.raises(UsageError):
+            store.init(0, w)  # duplicate
+        with pytest.raises(UsageError):
+            store.init(5, w)  # out of range
+
+    kv_ranks(1, 1, KvConfig("funnel", 1, 2), transport, None, body)
+
+
+def test_k_init_broadcasts_in_key_order(gpu):
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+    K = 4
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.ones(3))) for _ in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+
+    kv_ranks(2, 4, KvConfig("depcha", 1, K), transport, sink, body)
+    ev = sink.snapshot()
+    assert sum(1 for e in ev if e["event"] == "coll_matched" and e["kind"] == "broadcast") == K
+    for rank in range(2):
+        enq = enqueued(ev, rank)
+        assert [(e["kind"], e["comm"], e["seq"], e["key"]) for e in enq] == \
+            [("broadcast", 0, k, k) for k in range(K)]
+
+
+def test_funnel_push_leaves_global_sum_in_comm_buf(gpu):
+    transport = Transport.local(2, 5000)
+    sums = [None, None]
+
+    def body(rank, eng, store):
+        store.init(0, slot(eng, t64(np.zeros(2))))
+        eng.wait_all()
+        g = slot(eng, t64([1.0, 2.0] if rank == 0 else [3.0, 4.0]))
+        store.push(0, g)
+        sums[rank] = store.comm_buf(0).numpy()
+
+    kv_ranks(2, 2, KvConfig("funnel", 1, 1), transport, None, body)
+    for s in sums:
+        np.testing.assert_array_equal(s, [4.0, 6.0])
+
+
+def test_concom_hashes_keys_onto_extra_communicators(gpu):
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(4))) for _ in range(2)]
+        gs = [slot(eng, t64(np.full(4, rank + 1.0))) for _ in range(2)]
+        for k in range(2):
+            store.init(k, ws[k])
+        eng.wait_all()
+        store.push([0, 1], gs)
+        store.barrier()
+        assert store.outstanding_in_flight() == 0
+
+    kv_ranks(2, 4, KvConfig("concom", 2, 2), transport, sink, body)
+    ars = [e for e in enqueued(sink.snapshot()) if e["kind"] == "allreduce"]
+    assert ars and all(e["comm"] == 1 + e["key"] for e in ars)
+
+
+def test_depcha_push_issues_no_collective_pull_carries_it(gpu):
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+    outs = [None, None]
+    after_push = []
+
+    def body(rank, eng, store):
+        store.init(0, slot(eng, t64(np.zeros(3))))
+        eng.wait_all()
+        g = slot(eng, t64(np.full(3, 1.5 if rank == 0 else 2.0)))
+        store.push(0, g)
+        eng.wait_all()
+        if rank == 0:
+            after_push.append(sum(1 for e in sink.snapshot() if e.get("kind") == "allreduce" and e["rank"] == 0))
+        out = slot(eng, t64(np.zeros(3)))
+        store.pull(0, out)
+        eng.wait_all()
+        outs[rank] = out.value.cpu().numpy()
+
+    kv_ranks(2, 2, KvConfig("depcha", 1, 1), transport, sink, body)
+    assert after_push == [0]
+    for o in outs:
+        np.testing.assert_array_equal(o, [3.5, 3.5, 3.5])
+
+
+def test_pull_requires_push_and_shapes_are_validated(gpu):
+    transport = Transport.local(1, 5000)
+
+    def body(rank, eng, store):
+        store.init(0, slot(eng, t64(np.zeros(2))))
+        eng.wait_all()
+        with pytest.raises(UsageError):
+            store.pull(0, slot(eng, t64(np.zeros(2))))
+        with pytest.raises(UsageError):
+            store.push(0, slot(eng, t64(np.zeros(3))))
+        with pytest.raises(UsageError):
+            store.push(7, slot(eng, t64(np.zeros(3))))
+
+    kv_ranks(1, 1, KvConfig("funnel", 1, 1), transport, None, body)
+
+
+def test_barrier_is_noop_outside_concom(gpu):
+    sink = TraceSink()
+    transport = Transport.local(1, 5000, sink)
+
+    def body(rank, eng, store):
+        before = sink.count()
+        store.barrier()
+        assert sink.count() == before
+
+    kv_ranks(1, 1, KvConfig("funnel", 1, 1), transport, sink, body)
+
+
+def test_concom_barrier_drains_in_flight_counter(gpu):
+    transport = Transport.local(2, 5000)
+    transport.set_inject_latency(30000)
+    nonzero = []
+    sums = [None, None]
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(4))) for _ in range(2)]
+        gs = [slot(eng, t64(np.full(4, rank + 1.0))) for _ in range(2)]
+        for k in range(2):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for k in range(2):
+            store.push(k, gs[k])
+        if store.outstanding_in_flight() > 0:
+            nonzero.append(rank)
+        store.barrier()
+        assert store.outstanding_in_flight() == 0
+        store.barrier()
+        sums[rank] = store.comm_buf(0).numpy()
+
+    kv_ranks(2, 4, KvConfig("concom", 2, 2), transport, None, body)
+    assert len(nonzero) >= 1
+    for s in sums:
+        np.testing.assert_array_equal(s, np.full(4, 3.0))
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+@pytest.mark.parametrize("R", [2, 4])
+def test_aggregation_correctness(gpu, mode, R):
+    """test_kvstore.cpp:290-330: seeds 1000 + rank*K + k; the reference holds
+    1e-12, the device path is bit-exact (rank-order fp64 sum)."""
+    K = 3
+    transport = Transport.local(R, 5000)
+    outs = [[None] * K for _ in range(R)]
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(6))) for _ in range(K)]
+        gs = [slot(eng, t64(O.random_uniform(6, 1000 + rank * K + k))) for k in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for k in range(K):
+            store.push(k, gs[k])
+        for k in range(K):
+            store.pull(k, gs[k])
+        store.barrier()
+        eng.wait_all()
+        for k in range(K):
+            outs[rank][k] = gs[k].value.cpu().numpy()
+
+    kv_ranks(R, 4, KvConfig(mode, 2, K), transport, None, body)
+    for k in range(K):
+        exp = O.rank_order_sum([O.random_uniform(6, 1000 + r * K + k) for r in range(R)], "f64")
+        for r in range(R):
+            np.testing.assert_array_equal(outs[r][k], exp)
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha"])
+def test_order_consistency(gpu, mode):
+    """test_kvstore.cpp:332-371: world call sequence == key order on every rank."""
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+    K, iters = 8, 3
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(5))) for _ in range(K)]
+        gs = [slot(eng, t64(np.full(5, rank + 1.0))) for _ in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for _ in range(iters):
+            for k in range(K):
+                store.push(k, gs[k])
+            for k in range(K):
+                store.pull(k, gs[k])
+            eng.wait_all()
+
+    kv_ranks(2, 4, KvConfig(mode, 1, K), transport, sink, body)
+    per = [[e["key"] for e in enqueued(sink.snapshot(), r) if e["comm"] == 0 and e["kind"] == "allreduce"]
+           for r in range(2)]
+    assert len(per[0]) == K * iters
+    assert per[0] == per[1] == [k for _ in range(iters) for k in range(K)]
+
+
+def test_window_discipline_concom(gpu):
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+    K, outstanding = 8, 2
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(5))) for _ in range(K)]
+        gs = [slot(eng, t64(np.full(5, rank + 1.0))) for _ in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        since = 0
+        for k in range(K):
+            store.push(k, gs[k])
+            store.pull(k, gs[k])
+            since += 1
+            if since == outstanding:
+                store.barrier()
+                since = 0
+        if since:
+            store.barrier()
+        eng.wait_all()
+
+    kv_ranks(2, 4, KvConfig("concom", outstanding, K), transport, sink, body)
+    for rank in range(2):
+        window = []
+        for e in enqueued(sink.snapshot(), rank):
+            if e["kind"] == "allreduce":
+                window.append(e["comm"])
+                assert len(window) <= outstanding
+                assert len(set(window)) == len(window)
+            elif e["kind"] == "barrier":
+                window = []
+
+
+def test_funnel_serialization(gpu):
+    """test_kvstore.cpp:420-454: at most one in-flight collective per rank."""
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+    K = 6
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(4))) for _ in range(K)]
+        gs = [slot(eng, t64(np.full(4, rank + 1.0))) for _ in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for k in range(K):
+            store.push(k, gs[k])
+            store.pull(k, gs[k])
+        eng.wait_all()
+
+    kv_ranks(2, 4, KvConfig("funnel", 1, K), transport, sink, body)
+    for rank in range(2):
+        depth = 0
+        for e in sink.snapshot():
+            if e["rank"] != rank:
+                continue
+            if e["event"] == "coll_enqueued":
+                depth += 1
+                assert depth <= 1
+            elif e["event"] == "coll_done":
+                depth -= 1
+
+
+def test_shape_disagreement_surfaces_at_init_broadcast(gpu):
+    transport = Transport.local(2, 5000)
+    got = []
+
+    def body(rank, eng, store):
+        w = slot(eng, t64(np.zeros(4 if rank == 0 else 6)))
+        store.init(0, w)
+        try:
+            eng.wait_all()
+        except MismatchError:
+            got.append(rank)
+
+    kv_ranks(2, 2, KvConfig("funnel", 1, 1), transport, None, body)
+    assert sorted(got) == [0, 1]
+
+
+def test_naive_single_thread_never_misorders(gpu):
+    for seed in range(1, 4):
+        transport = Transport.local(2, 2000)
+        K = 4
+
+        def body(rank, eng, store):
+            ws = [slot(eng, t64(np.zeros(3))) for _ in range(K)]
+            gs = [slot(eng, t64(np.full(3, rank + 1.0 + seed))) for _ in range(K)]
+            for k in range(K):
+                store.init(k, ws[k])
+            eng.wait_all()
+            for _ in range(2):
+                for k in range(K):
+                    store.push(k, gs[k])
+                for k in range(K):
+                    store.pull(k, gs[k])
+                eng.wait_all()
+
+        errs = kv_ranks(2, 1, KvConfig("naive", 1, K), transport, None, body)
+        assert all(e is None for e in errs)
+
+
+def test_naive_hazard_and_depcha_safety(gpu):
+    """acceptance.cpp:211-238: naive (4 engine threads) trips the ledger in
+    >= 1 of N runs; depcha on the same shape never errors.  The hazard is
+    caught by the matching ledger BEFORE any device collective is enqueued."""
+    hazards, depcha_errors = 0, 0
+    for seed in range(1, 11):
+        for mode in ("naive", "depcha"):
+            transport = Transport.local(2, 300)
+            K = 8
+
+            def body(rank, eng, store):
+                ws = [slot(eng, t64(np.zeros(3))) for _ in range(K)]
+                gs = [slot(eng, t64(np.full(3, float(rank)))) for _ in range(K)]
+                for k in range(K):
+                    store.init(k, ws[k])
+                eng.wait_all()
+                for _ in range(2):
+                    for k in range(K):
+                        store.push(k, gs[k])
+                    for k in range(K):
+                        store.pull(k, gs[k])
+                    eng.wait_all()
+
+            errs = kv_ranks(2, 4, KvConfig(mode, 1, K), transport, None, body,
+                            swallow=(MismatchError, DeadlockTimeout))
+            bad = any(isinstance(e, (MismatchError, DeadlockTimeout)) for e in errs)
+            if mode == "naive":
+                hazards += bad
+            else:
+                depcha_errors += bad
+        if hazards and seed >= 3:
+            break
+    assert hazards >= 1
+    assert depcha_errors == 0
+
+
+# ------------------------------------------------------------- golden parity
+
+def _seq(events, rank):
+    return [f"{e['kind']}:{e['comm']}:{e['seq']}:{e.get('key', -1)}" for e in enqueued(events, rank)]
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+def test_issue_sequences_match_reference_golden(gpu, mode):
+    """Per-rank collective issue order of the trainer loop shape
+    (trainer.cpp:112-141), K=8 keys, 2 iterations -- identical to the
+    sequences the reference emitted (tests/golden/issue_kv.json).  ConCom:
+    per-communicator sequences (the interleaving across comms is not ordered
+    in the reference either)."""
+    gold = json.loads((GOLD / "issue_kv.json").read_text())[mode]
+    K, iters, outstanding = gold["K"], gold["iters"], gold["outstanding"]
+    sink = TraceSink()
+    transport = Transport.local(2, 5000, sink)
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(np.zeros(5))) for _ in range(K)]
+        gs = [slot(eng, t64(np.full(5, rank + 1.0))) for _ in range(K)]
+        src = [t64(np.full(5, rank + 1.0)) for _ in range(K)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for _ in range(iters):
+            for k in reversed(range(K)):
+                producer(eng, src[k], gs[k], k)
+            if mode in ("funnel", "concom"):
+                since = 0
+                for k in range(K):
+                    store.push(k, gs[k])
+                    store.pull(k, gs[k])
+                    sgd_op(eng, ws[k], gs[k], 0.1, 1 / 128, k)
+                    if mode == "concom":
+                        since += 1
+                        if since == outstanding:
+                            store.barrier()
+                            since = 0
+                if mode == "concom" and since:
+                    store.barrier()
+            else:
+                for k in range(K):
+                    store.push(k, gs[k])
+                for k in range(K):
+                    store.pull(k, gs[k])
+                    sgd_op(eng, ws[k], gs[k], 0.1, 1 / 128, k)
+            eng.wait_all()
+
+    kv_ranks(2, 4, KvConfig(mode, outstanding, K), transport, sink, body)
+    ev = sink.snapshot()
+    for r in range(2):
+        mine, ref = _seq(ev, r), gold["per_rank"][str(r)]
+        if mode == "concom":
+            for comm in {s.split(":")[1] for s in ref}:
+                assert [s for s in mine if s.split(":")[1] == comm] == \
+                    [s for s in ref if s.split(":")[1] == comm]
+        else:
+            assert mine == ref
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("fused", [False, True])
+def test_train_steps_bit_exact_vs_reference(gpu, mode, R, fused):
+    """3 iterations of backward -> push -> pull -> sgd through the device
+    KvStore reproduce the reference KvStore's final fp64 weights bit-for-bit
+    on every rank (golden: tests/golden/train_steps.npz).  fused=True uses
+    pull_update (kernel (c) reading the reduced buffer directly)."""
+    gold = np.load(GOLD / "train_steps.npz")
+    sizes = [int(s) for s in gold["sizes"]]
+    lr = float(gold["lr"])
+    K = len(sizes)
+    rescale = 1.0 / (64 * R)
+    outstanding = 2 if mode == "concom" else 1
+    transport = Transport.local(R, 10000)
+    finals = [[None] * K for _ in range(R)]
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n)))
+              for k, n in enumerate(sizes)]
+        gs = [slot(eng, t64(np.zeros(n))) for n in sizes]
+        src = [t64(O.random_uniform(n, 1000 + rank * K + k)) for k, n in enumerate(sizes)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        for _ in range(3):
+            for k in reversed(range(K)):
+                producer(eng, src[k], gs[k], k)
+            if mode in ("funnel", "concom"):
+                since = 0
+                for k in range(K):
+                    store.push(k, gs[k])
+                    if fused:
+                        store.pull_update(k, ws[k], lr, rescale)
+                    else:
+                        store.pull(k, gs[k])
+                        sgd_op(eng, ws[k], gs[k], lr, rescale, k)
+                    if mode == "concom":
+                        since += 1
+                        if since == outstanding:
+                            store.barrier()
+                            since = 0
+                if mode == "concom" and since:
+                    store.barrier()
+            else:
+                store.push(list(range(K)), gs)
+                if fused:
+                    store.pull_update(list(range(K)), ws, lr, rescale)
+                else:
+                    for k in range(K):
+                        store.pull(k, gs[k])
+                        sgd_op(eng, ws[k], gs[k], lr, rescale, k)
+            eng.wait_all()
+        for k in range(K):
+            finals[rank][k] = ws[k].value.cpu().numpy()
+
+    kv_ranks(R, 4, KvConfig(mode, outstanding, K), transport, None, body)
+    for r in range(R):
+        for k in range(K):
+            np.testing.assert_array_equal(finals[r][k], gold[f"{mode}_R{R}_r{r}_k{k}"])
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+@pytest.mark.parametrize("comm_dtype", ["f32", "bf16"])
+def test_fusion_buckets_match_unbucketed(gpu, mode, comm_dtype):
+    """Fusion buckets (kernel (a) packs a bucket per launch, one collective per
+    bucket, kernel (c) updates a bucket per launch) give the same weights as
+    the 1:1 map; the key -> (bucket, offset) map is the documented greedy
+    one."""
+    from schedule import bucket_map
+    R, sizes = 2, [3, 1000, 5, 70000, 64, 129, 4096, 1]
+    K = len(sizes)
+    cdt = api.F32 if comm_dtype == "f32" else api.BF16
+    bucket_bytes = 64 * 1024
+    results = {}
+    for bb in (0, bucket_bytes):
+        transport = Transport.local(R, 10000)
+        out = [[None] * K for _ in range(R)]
+        maps = [None] * R
+
+        def body(rank, eng, store):
+            ws = [slot(eng, torch.from_numpy(O.random_uniform(n, k).astype(np.float32)).cuda())
+                  for k, n in enumerate(sizes)]
+            gs = [slot(eng, torch.from_numpy(O.random_uniform(n, 50 + rank * K + k).astype(np.float32)).cuda())
+                  for k, n in enumerate(sizes)]
+            for k in range(K):
+                store.init(k, ws[k])
+            eng.wait_all()
+            order = list(reversed(range(K)))  # gradient-ready order
+            if mode == "depcha":
+                store.push(order, [gs[k] for k in order])
+                store.pull_update(order, [ws[k] for k in order], 0.1, 0.01, 0.9)
+            else:
+                # per bucket: push its keys, then pull them
+                groups = bucket_map(sizes, 4 if cdt == api.F32 else 2, bb, issue_order=1)[2]
+                since = 0
+                for keys in groups:
+                    store.push(keys, [gs[k] for k in keys])
+                    store.pull_update(keys, [ws[k] for k in keys], 0.1, 0.01, 0.9)
+                    if mode == "concom":
+                        since += 1
+                        if since == 2:
+                            store.barrier()
+                            since = 0
+                if mode == "concom" and since:
+                    store.barrier()
+            eng.wait_all()
+            for k in range(K):
+                out[rank][k] = ws[k].value.cpu().numpy()
+            maps[rank] = [store.key_map(k) for k in range(K)]
+
+        kv_ranks(R, 4, KvConfig(mode, 2, K, comm_dtype=cdt, bucket_bytes=bb, issue_order=1),
+                 transport, None, body)
+        results[bb] = out
+        if bb:
+            exp_bucket, exp_off, _ = bucket_map(sizes, 4 if cdt == api.F32 else 2, bb, issue_order=1)
+            for r in range(R):
+                assert maps[r] == list(zip(exp_bucket, exp_off))
+    for r in range(R):
+        for k in range(K):
+            np.testing.assert_array_equal(results[0][r][k], results[bucket_bytes][r][k])
+    # value check against the fp64 oracle of the same (rounded) inputs
+    for k, n in enumerate(sizes):
+        g = [O.random_uniform(n, 50 + r * K + k).astype(np.float32) for r in range(R)]
+        if cdt == api.BF16:
+            g = [O.bf16_bits_to_f32(O.f32_to_bf16_bits(x)) for x in g]
+        s = O.rank_order_sum([x.astype(np.float64) for x in g], "f64")
+        w0 = O.random_uniform(n, k).astype(np.float32).astype(np.float64)
+        ew, _ = O.sgd_update(w0, s, 0.1, 0.01, 0.9, np.zeros(n))
+        tol = 1e-6 if cdt == api.F32 else 1e-2
+        scale = np.abs(w0) + 0.1 * 0.01 * np.sum([np.abs(x) for x in g], axis=0)
+        assert np.all(np.abs(results[bucket_bytes][0][k] - ew) <= tol * scale + 1e-7)
