@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py -- aggregated gradient GB/s and exposed comm ms/iter (BASELINE.json).
+
+Workload (N=1 default, BASELINE.json configs[1]): the ResNet-50 gradient set
+(161 keys, 25,557,032 fp32 params, torchvision parameter order) under DepCha,
+fusion buckets of 25 MiB grouped in gradient-ready (descending) order, SGD
+with momentum 0.9.  One "step" = one pass of the hot path over every key:
+push (kernel (a) packs each bucket) -> allreduce (NCCL, one ordered stream,
+chained by the DepCha dummy tag) -> fused pull+update (kernel (c) reads the
+reduced bucket and updates weights + momentum in place).
+
+  value          whole-job aggregated gradient GB/s = N x gradient bytes per
+                 rank / device step time (max over ranks), gradients resident
+                 in HBM; inputs (gradients + weights + momentum + buckets,
+                 ~409 MB/rank) exceed the 126 MB L2, so no flush is needed.
+  e2e            same metric through the C-ABI with HOST buffers: every step
+                 copies the gradients H2D from pinned memory, runs the path,
+                 and reads the weight checksum back D2H (wall clock).
+  exposed_comm   T(synthetic backward + aggregation) - T(synthetic backward +
+                 local update), per iteration, CUDA events, max over ranks.
+  roofline       dominant kernel of the step, CUDA-event timed per launch on
+                 its own stream, algorithmic bytes / duration vs measured HBM.
+  cpu_baseline   the reference (oracle/_ref, compiled from /root/reference)
+                 timed on this host's cores on a bounded sample (rank 0, N=1).
+
+`--impl reference` times the reference's own CPU path (oracle/_ref) instead.
+For N > 1 launch with torchrun; one process per GPU, NCCL between them.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "aggregated gradient GB/s/GPU & exposed comm ms/iter at 1/2/4/8 B200"
+CONFIGS = {
+    # name: (keyset, mode, outstanding, dtype, bucket_mb, backward_ms)
+    "resnet50": ("resnet50", "depcha", 1, "fp32", 25, 24.0),
+    "alexnet": ("alexnet", "concom", 4, "fp32", 25, 20.0),
+    "resnet152": ("resnet152", "depcha", 1, "bf16", 25, 60.0),
+    "inception_v3": ("inception_v3", "depcha", 1, "bf16", 25, 30.0),
+    "stress": ("stress", "depcha", 1, "fp32", 64, 0.0),
+    "uniform16": ("uniform16x1048576", "funnel", 1, "fp32", 0, 0.0),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
+    p.add_argument("--mode", default=None, choices=["funnel", "depcha", "concom"])
+    p.add_argument("--outstanding", type=int, default=None)
+    p.add_argument("--bucket-mb", type=float, default=None)
+    p.add_argument("--issue-order", default="descending", choices=["ascending", "descending"])
+    p.add_argument("--momentum", type=float, default=0.9)
+    p.add_argument("--backward-ms", type=float, default=None)
+    p.add_argument("--engine-threads", type=int, default=4)
+    p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def wait_first(self, timeout: float = 5.0):
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------- reference
+
+def run_reference(args, keys, mode, outstanding, world):
+    """The reference's own CPU path (Engine + KvStore + Transport, compiled
+    from /root/reference into oracle/_ref) on the host cores."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ctypes as C
+    import _oracle as O  # checker / reference loader (test infrastructure)
+
+    R = O.ref_lib()
+    if R is None:
+        return None
+    ncores = os.cpu_count() or 1
+    ranks = max(1, world)
+    threads = max(2, ncores // ranks)
+    sizes = (C.c_int64 * len(keys))(*keys)
+    stats = (C.c_double * 2)()
+    rc = R.ref_bench(mode.encode(), ranks, threads, outstanding, len(keys), sizes, 1, args.cpu_steps, 0,
+                     0.1, 1.0 / (64 * ranks), stats)
+    if rc != 0:
+        raise RuntimeError(R.ref_last_error().decode())
+    ms = stats[0]
+    bytes_rank = stats[1]
+    return {"ms_per_step": ms, "value": ranks * bytes_rank / (ms * 1e6), "per_rank": bytes_rank / (ms * 1e6),
+            "cores": min(ncores, ranks * (threads + 1)), "ranks": ranks, "threads": threads,
+            "bytes_per_rank": bytes_rank}
+
+
+def reference_main(args, cfg_name, keys, mode, outstanding, config):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    ref = run_reference(args, keys, mode, outstanding, world)
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcollsim_ref.so not built"}))
+        return
+    line = {
+        "metric": METRIC, "impl": "reference", "value": round(ref["value"], 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.cpu_steps, "warmup": 1, "ms_per_step": round(ref["ms_per_step"], 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (random_uniform seeds 1000+r*K+k)", "config": config,
+        "cpu_baseline": {"value": round(ref["value"], 4), "unit": "GB/s", "cores": ref["cores"],
+                         "kind": "reference",
+                         "sample": f"{len(keys)} keys, {ref['ranks']} rank threads x {ref['threads']} engine "
+                                   f"threads, fp64, {args.cpu_steps} iterations after 1 warm-up"},
+        "e2e": {"value": round(ref["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+
+def main():
+    args = parse()
+    keyset, mode, outstanding, dtype, bucket_mb, bwd_ms = CONFIGS[args.config]
+    mode = args.mode or mode
+    outstanding = args.outstanding or outstanding
+    bucket_mb = args.bucket_mb if args.bucket_mb is not None else bucket_mb
+    bwd_ms = args.backward_ms if args.backward_ms is not None else bwd_ms
+    from paper_1802_06949_b200 import keysets
+    keys = keysets.load(keyset)
+    rank, local_rank, world = dist_env()
+    config = {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
+              "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
+              "issue_order": args.issue_order, "momentum": args.momentum, "parallelism": f"dp{world}",
+              "l2": "inputs larger than L2 (no flush)"}
+    if args.impl == "reference":
+        return reference_main(args, args.config, keys, mode, outstanding, config)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1802_06949_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    name = [f"collsim_{os.getpid()}_{int(time.time() * 1e6) % 10**9}"]
+    if world > 1:
+        dist.broadcast_object_list(name, src=0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    dt = {"fp32": api.F32, "bf16": api.BF16}[dtype]
+    transport = api.Transport.nccl(name[0], world, rank, local_rank, 120000)
+    comms_main = api.create_communicators(transport, outstanding) if mode == "concom" else []
+    comms_e2e = api.create_communicators(transport, outstanding) if (mode == "concom" and not args.no_extras) else []
+    engine = api.Engine(args.engine_threads, rank, None, local_rank)
+    common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
+                  bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
+                  outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
+                  backward_ns=int(bwd_ms * 1e6), comm_priority=-5)
+    model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, **common)
+    model.init()
+    info = model.info()
+    gbytes = info["grad_bytes"]
+    COMM = api.SynthModel.COMM
+    BWD = api.SynthModel.BACKWARD
+    LOCAL = api.SynthModel.LOCAL_UPDATE
+
+    # ---- headline: aggregation steps, gradients resident in HBM
+    model.run(args.warmup, COMM)
+    barrier()
+    api.host_profile(reset=True)
+    l0 = api.launch_count()
+    with Clocks(local_rank) as clk:
+        clk.wait_first()
+        ms = model.run(args.steps, COMM)
+        launches = api.launch_count() - l0
+        host_ms = model.last_host_ms()
+        if os.environ.get("CSB_HOST_PROFILE") == "1":
+            print(json.dumps({"host_profile_per_step": {k: round(v["us"] / args.steps, 2)
+                                                        for k, v in api.host_profile().items()}}),
+                  file=sys.stderr)
+        # the timed region is short; keep the same steps running ~0.5 s so
+        # the sampler sees the clocks under this exact load
+        t_end = time.time() + 0.5
+        while time.time() < t_end:
+            model.run(args.steps, COMM)
+    barrier()
+    ms = max_over_ranks(ms)
+    step_ms = ms / args.steps
+    per_gpu = gbytes / (step_ms * 1e6)
+    value = world * per_gpu
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype.replace("fp", "f"),
+            "data": "synthetic (random_uniform seeds 1000+r*K+k; torchvision ResNet-50 key sizes)",
+            "config": config, "per_gpu_gbs": round(per_gpu, 3), "grad_bytes_per_rank": gbytes,
+            "buckets": info["num_buckets"], "gpu_launches": launches,
+            "host_dispatch_ms_per_step": round(host_ms / args.steps, 4),
+            "clocks": {**clk.summary(), "window": "timed region + 0.5 s of the same steps"}}
+
+    if not args.no_extras:
+        # ---- exposed communication under the synthetic backward
+        n_exp = max(3, min(args.steps, 10))
+        model.run(1, BWD | COMM)
+        barrier()
+        t_full = max_over_ranks(model.run(n_exp, BWD | COMM)) / n_exp
+        barrier()
+        model.run(1, BWD | LOCAL)
+        barrier()
+        t_comp = max_over_ranks(model.run(n_exp, BWD | LOCAL)) / n_exp
+        line["exposed_comm_ms"] = round(t_full - t_comp, 4)
+        line["step_with_backward_ms"] = round(t_full, 4)
+        line["backward_plus_update_ms"] = round(t_comp, 4)
+        line["exposed_frac"] = round((t_full - t_comp) / t_full, 4) if t_full > 0 else None
+        line["synthetic_backward_ms"] = bwd_ms
+
+        # ---- roofline of the dominant kernel (CUDA events on the launch stream)
+        api.profile_reset()
+        api.profile_enable(True)
+        model.run(max(3, min(args.steps, 10)), COMM)
+        api.profile_enable(False)
+        kstats = {k: api.profile_collect(k) for k in ("pack", "sum", "sgd")}
+        dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
+        ks = kstats[dom]
+        pk = peaks()
+        peak = pk.get("hbm_gbs", 6650.0)
+        achieved = ks["bytes"] / (ks["total_ms"] * 1e6) if ks["total_ms"] > 0 else 0.0
+        line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                            "launches": ks["launches"],
+                            "avg_launch_us": round(1000 * ks["total_ms"] / max(1, ks["launches"]), 2),
+                            "bytes_per_launch": round(ks["bytes"] / max(1, ks["launches"])),
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback",
+                            "kernels": {k: {"launches": v["launches"],
+                                            "ms_per_step": round(v["total_ms"] / max(3, min(args.steps, 10)), 4),
+                                            "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}
+                                        for k, v in kstats.items()}}
+
+        # ---- end to end through the C ABI with host buffers
+        model_e2e = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_e2e,
+                                   host_source=True, **{**common, "backward_ns": 0})
+        model_e2e.init()
+        model_e2e.run_e2e(2, BWD | COMM)
+        barrier()
+        wall = max_over_ranks(model_e2e.run_e2e(args.steps, BWD | COMM))
+        e2e_step = wall / args.steps
+        line["e2e"] = {"value": round(world * gbytes / (e2e_step * 1e6), 3), "unit": "GB/s",
+                       "h2d_bytes_per_step": model_e2e.info()["h2d_bytes_per_step"], "d2h_bytes_per_step": 8,
+                       "ms_per_step": round(e2e_step, 4)}
+        model_e2e.close()
+
+        # ---- CPU baseline: the reference on this host, bounded sample
+        if world == 1 and rank == 0:
+            try:
+                ref = run_reference(args, keys, mode, outstanding, 1)
+            except Exception as e:  # reported, not fatal
+                ref = None
+                line["cpu_baseline"] = {"error": str(e)}
+            if ref:
+                line["cpu_baseline"] = {
+                    "value": round(ref["per_rank"], 4), "unit": "GB/s", "cores": ref["cores"], "kind": "reference",
+                    "sample": f"{len(keys)} keys fp64, 1 rank thread x {ref['threads']} engine threads, "
+                              f"{args.cpu_steps} iterations after 1 warm-up (oracle/_ref = unmodified reference)",
+                    "ms_per_step": round(ref["ms_per_step"], 2)}
+    model.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier()
+    engine.close()
+    transport.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

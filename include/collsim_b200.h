@@ -202,6 +202,48 @@ int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems)
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
 int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);
 
+/* ------------------------------------------ synthetic training step */
+/* The reference trainer's loop shapes (trainer.cpp:112-141) over a key set,
+ * with a synthetic backward (one producer op per key, descending keys). */
+typedef struct cs_synth* cs_synth_t;
+typedef struct cs_synth_config {
+  int mode;               /* CS_KV_* */
+  int w_dtype, g_dtype, comm_dtype;
+  uint64_t bucket_bytes;
+  int issue_order;        /* 0 ascending keys, 1 descending (gradient-ready order) */
+  int outstanding;
+  double lr, rescale, momentum;
+  uint64_t backward_ns;   /* total synthetic backward device time per step */
+  int backward_ctas;      /* 0: one CTA per SM */
+  int fused_update;       /* 1: pull_update (kernel (c) on the reduced bucket) */
+  int comm_priority;
+  int host_source;        /* 1: gradients copied from pinned host memory each step */
+} cs_synth_config;
+enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
+int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,
+                    const uint64_t* sizes, int num_keys, const int* concom_comms, int n_comms,
+                    cs_synth_t* out);
+int cs_synth_destroy(cs_synth_t s);
+int cs_synth_init(cs_synth_t s);
+int cs_synth_step(cs_synth_t s, int flags);
+/* device time (CUDA events spanning every lane) of `steps` steps */
+int cs_synth_run(cs_synth_t s, int steps, int flags, double* device_ms);
+/* host wall time of `steps` steps, each ending with the result on the host */
+int cs_synth_run_e2e(cs_synth_t s, int steps, int flags, double* wall_ms);
+int cs_synth_checksum(cs_synth_t s, double* out);
+int cs_synth_info(cs_synth_t s, uint64_t* grad_bytes, uint64_t* h2d_bytes_per_step, int* num_buckets);
+/* host time the last cs_synth_run spent dispatching (enqueue-bound check) */
+int cs_synth_last_host_ms(cs_synth_t s, double* out);
+
+/* ------------------------------------------------ launch accounting */
+enum { CS_KERNEL_PACK = 0, CS_KERNEL_SUM = 1, CS_KERNEL_SGD = 2, CS_KERNEL_SYNTH = 3, CS_KERNEL_CHECKSUM = 4 };
+int cs_launch_count(uint64_t* out); /* kernels of this library launched so far */
+int cs_profile_enable(int on);      /* per-launch CUDA-event timing on the launch stream */
+int cs_profile_collect(int kind, uint64_t* launches, double* total_ms, double* bytes);
+int cs_profile_reset(void);
+/* host-side section timers (enabled by CSB_HOST_PROFILE=1): JSON into buf */
+int cs_host_profile(char* buf, int cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

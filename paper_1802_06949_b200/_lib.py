@@ -107,7 +107,33 @@ SIGNATURES = {
     "cs_kv_key_map": [_P, _I, _PI, _PU64],
     "cs_kv_num_buckets": [_P, _PI],
     "cs_kv_bucket_lane": [_P, _I, _PI],
+    "cs_synth_create": [_P, _P, _I, _I, C.c_void_p, _PU64, _I, _PI, _I, C.POINTER(_P)],
+    "cs_synth_destroy": [_P],
+    "cs_synth_init": [_P],
+    "cs_synth_step": [_P, _I],
+    "cs_synth_run": [_P, _I, _I, C.POINTER(C.c_double)],
+    "cs_synth_run_e2e": [_P, _I, _I, C.POINTER(C.c_double)],
+    "cs_synth_checksum": [_P, C.POINTER(C.c_double)],
+    "cs_synth_info": [_P, _PU64, _PU64, _PI],
+    "cs_synth_last_host_ms": [_P, C.POINTER(C.c_double)],
+    "cs_launch_count": [_PU64],
+    "cs_profile_enable": [_I],
+    "cs_profile_collect": [_I, _PU64, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "cs_profile_reset": [],
+    "cs_host_profile": [C.c_char_p, _I, _I],
 }
+
+
+class SynthConfigC(C.Structure):
+    _fields_ = [("mode", C.c_int), ("w_dtype", C.c_int), ("g_dtype", C.c_int), ("comm_dtype", C.c_int),
+                ("bucket_bytes", C.c_uint64), ("issue_order", C.c_int), ("outstanding", C.c_int),
+                ("lr", C.c_double), ("rescale", C.c_double), ("momentum", C.c_double),
+                ("backward_ns", C.c_uint64), ("backward_ctas", C.c_int), ("fused_update", C.c_int),
+                ("comm_priority", C.c_int), ("host_source", C.c_int)]
+
+
+CS_STEP_BACKWARD, CS_STEP_COMM, CS_STEP_LOCAL_UPDATE, CS_STEP_CHECKSUM = 1, 2, 4, 8
+KERNEL_KINDS = {"pack": 0, "sum": 1, "sgd": 2, "synth": 3, "checksum": 4}
 _RESTYPE = {"cs_last_error": C.c_char_p, "cs_status_name": C.c_char_p}
 
 

@@ -473,3 +473,98 @@ def synth_backward(src: int, dst: int, n: int, dt: int, spin_ns: int = 0, ctas: 
 
 def checksum(x: int, n: int, dt: int, out_dev: int, stream: int = 0) -> None:
     check(lib.cs_checksum(x, n, dt, out_dev, stream))
+
+
+# --------------------------------------------------- synthetic training step
+
+class SynthModel:
+    """The reference trainer's loop shapes (trainer.cpp:112-141) over a key
+    set with a synthetic backward, driven entirely in the native library."""
+
+    BACKWARD, COMM, LOCAL_UPDATE, CHECKSUM = 1, 2, 4, 8
+
+    def __init__(self, engine: Engine, transport: Transport, rank: int, nranks: int, sizes,
+                 mode: str = "depcha", w_dtype: int = F32, g_dtype: int = F32, comm_dtype: int = F32,
+                 bucket_bytes: int = 0, issue_order: int = 0, outstanding: int = 1, lr: float = 0.1,
+                 rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
+                 backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0,
+                 host_source: bool = False, concom_comms: Sequence[int] = ()):
+        cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
+                                outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
+                                int(fused_update), comm_priority, int(host_source))
+        sz = (C.c_uint64 * len(sizes))(*sizes)
+        comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
+        h = C.c_void_p()
+        check(lib.cs_synth_create(engine.h, transport.h, rank, nranks, C.byref(cfg), sz, len(sizes),
+                                  comms, len(concom_comms), C.byref(h)))
+        self.h = h
+        self.engine = engine
+        self.transport = transport
+
+    def init(self) -> None:
+        check(lib.cs_synth_init(self.h))
+
+    def step(self, flags: int) -> None:
+        check(lib.cs_synth_step(self.h, flags))
+
+    def run(self, steps: int, flags: int) -> float:
+        ms = C.c_double()
+        check(lib.cs_synth_run(self.h, steps, flags, C.byref(ms)))
+        return ms.value
+
+    def run_e2e(self, steps: int, flags: int) -> float:
+        ms = C.c_double()
+        check(lib.cs_synth_run_e2e(self.h, steps, flags, C.byref(ms)))
+        return ms.value
+
+    def checksum(self) -> float:
+        v = C.c_double()
+        check(lib.cs_synth_checksum(self.h, C.byref(v)))
+        return v.value
+
+    def last_host_ms(self) -> float:
+        v = C.c_double()
+        check(lib.cs_synth_last_host_ms(self.h, C.byref(v)))
+        return v.value
+
+    def info(self) -> dict:
+        g, h2d, nb = C.c_uint64(), C.c_uint64(), C.c_int()
+        check(lib.cs_synth_info(self.h, C.byref(g), C.byref(h2d), C.byref(nb)))
+        return {"grad_bytes": g.value, "h2d_bytes_per_step": h2d.value, "num_buckets": nb.value}
+
+    def close(self):
+        if self.h:
+            lib.cs_synth_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def launch_count() -> int:
+    n = C.c_uint64()
+    check(lib.cs_launch_count(C.byref(n)))
+    return n.value
+
+
+def profile_enable(on: bool) -> None:
+    check(lib.cs_profile_enable(int(on)))
+
+
+def profile_reset() -> None:
+    check(lib.cs_profile_reset())
+
+
+def host_profile(reset: bool = False) -> dict:
+    buf = C.create_string_buffer(4096)
+    check(lib.cs_host_profile(buf, 4096, int(reset)))
+    return json.loads(buf.value.decode())
+
+
+def profile_collect(kind: str) -> dict:
+    n, ms, b = C.c_uint64(), C.c_double(), C.c_double()
+    check(lib.cs_profile_collect(_lib.KERNEL_KINDS[kind], C.byref(n), C.byref(ms), C.byref(b)))
+    return {"launches": n.value, "total_ms": ms.value, "bytes": b.value}

@@ -8,8 +8,10 @@
 
 #include "collsim_b200.h"
 #include "engine.hpp"
+#include "hostprof.hpp"
 #include "kernels.hpp"
 #include "kvstore.hpp"
+#include "trainer.hpp"
 #include "transport.hpp"
 
 using namespace csb;
@@ -26,6 +28,9 @@ struct cs_transport {
 struct cs_kvstore {
   std::unique_ptr<KvStore> kv;
   Engine* engine;
+};
+struct cs_synth {
+  std::unique_ptr<SynthModel> m;
 };
 
 namespace {
@@ -447,6 +452,117 @@ int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane) {
   return guard([&] {
     CHECK_HANDLE(kv);
     *lane = kv->kv->bucket_lane(bucket);
+  });
+}
+
+// -------------------------------------------------------------- synth
+int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,
+                    const uint64_t* sizes, int num_keys, const int* concom_comms, int n_comms,
+                    cs_synth_t* out) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    CHECK_HANDLE(t);
+    CHECK_HANDLE(cfg);
+    if (num_keys < 1 || !sizes) throw ConfigError("synth: no keys");
+    if (cfg->mode < 0 || cfg->mode > 3) throw ConfigError("unknown kvstore mode");
+    SynthConfig c;
+    c.mode = static_cast<KvMode>(cfg->mode);
+    c.sizes.assign(sizes, sizes + num_keys);
+    c.wdt = cfg->w_dtype;
+    c.gdt = cfg->g_dtype;
+    c.cdt = cfg->comm_dtype;
+    c.bucket_bytes = cfg->bucket_bytes;
+    c.issue_order = cfg->issue_order;
+    c.outstanding = cfg->outstanding;
+    c.lr = cfg->lr;
+    c.rescale = cfg->rescale;
+    c.momentum = cfg->momentum;
+    c.backward_ns = cfg->backward_ns;
+    c.backward_ctas = cfg->backward_ctas;
+    c.fused = cfg->fused_update != 0;
+    c.comm_priority = cfg->comm_priority;
+    c.host_source = cfg->host_source != 0;
+    std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
+    auto h = std::make_unique<cs_synth>();
+    h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
+    *out = h.release();
+  });
+}
+int cs_synth_destroy(cs_synth_t s) {
+  return guard([&] { delete s; });
+}
+int cs_synth_init(cs_synth_t s) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    s->m->init();
+  });
+}
+int cs_synth_step(cs_synth_t s, int flags) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    s->m->enqueue_step(flags);
+  });
+}
+int cs_synth_run(cs_synth_t s, int steps, int flags, double* device_ms) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    *device_ms = s->m->run(steps, flags);
+  });
+}
+int cs_synth_run_e2e(cs_synth_t s, int steps, int flags, double* wall_ms) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    *wall_ms = s->m->run_e2e(steps, flags);
+  });
+}
+int cs_synth_checksum(cs_synth_t s, double* out) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    *out = s->m->checksum();
+  });
+}
+int cs_synth_info(cs_synth_t s, uint64_t* grad_bytes, uint64_t* h2d, int* num_buckets) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    if (grad_bytes) *grad_bytes = s->m->grad_bytes();
+    if (h2d) *h2d = s->m->h2d_bytes_per_step();
+    if (num_buckets) *num_buckets = s->m->num_buckets();
+  });
+}
+int cs_synth_last_host_ms(cs_synth_t s, double* out) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    *out = s->m->last_host_ms();
+  });
+}
+
+// ---------------------------------------------------- launch accounting
+int cs_launch_count(uint64_t* out) {
+  return guard([&] { *out = launch_count(); });
+}
+int cs_profile_enable(int on) {
+  return guard([&] { profile_enable(on != 0); });
+}
+int cs_profile_collect(int kind, uint64_t* launches, double* total_ms, double* bytes) {
+  return guard([&] {
+    KernelStats st = profile_collect(kind);
+    if (launches) *launches = st.launches;
+    if (total_ms) *total_ms = st.total_ms;
+    if (bytes) *bytes = st.bytes;
+  });
+}
+int cs_profile_reset(void) {
+  return guard([&] { profile_reset(); });
+}
+int cs_host_profile(char* buf, int cap, int reset) {
+  return guard([&] {
+    const std::string s = hostprof::report_json();
+    if (buf && cap > 0) {
+      const size_t n = std::min(static_cast<size_t>(cap - 1), s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = '\0';
+    }
+    if (reset) hostprof::reset();
   });
 }
 

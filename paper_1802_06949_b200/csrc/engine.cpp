@@ -6,8 +6,11 @@
 //   wait_for / wait_all / shutdown R/core/src/engine.cpp:217-246
 #include "engine.hpp"
 
+#include "hostprof.hpp"
+
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 
 namespace csb {
 
@@ -48,6 +51,7 @@ Engine::Engine(int num_worker_threads, int rank, TraceSink* trace, int device)
   if (num_worker_threads < 1) throw ConfigError("Engine: worker pool size must be >= 1");
   pool_ = std::make_shared<EventPool>();
   pool_->device = device;
+  if (const char* s = std::getenv("CSB_ENGINE_SPIN_US")) spin_ = std::chrono::microseconds(std::atoll(s));
   lanes_.reserve(kMaxLanes);
   if (device_ >= 0) {
     int count = 0;
@@ -159,12 +163,18 @@ OpId Engine::enqueue(std::unique_ptr<Operation> op, const std::vector<Tag>& read
                      const std::vector<Tag>& mutates) {
   OpId id;
   {
+    hostprof::Scope prof(hostprof::kEnqueue);
     std::lock_guard<std::mutex> lock(mu_);
     if (shut_down_ || stopping_) throw UsageError("Engine: push after shutdown");
-    for (const Tag& r : reads)
+    if (!reads.empty() && !mutates.empty()) {
+      std::vector<uint64_t> r;
+      r.reserve(reads.size());
+      for (const Tag& t : reads) r.push_back(t.id);
+      std::sort(r.begin(), r.end());
       for (const Tag& m : mutates)
-        if (r.id == m.id)
+        if (std::binary_search(r.begin(), r.end(), m.id))
           throw UsageError("Engine: a tag may not appear in both reads and mutates");
+    }
     for (const Tag& t : reads) var_for(t);
     for (const Tag& t : mutates) var_for(t);
 
@@ -235,7 +245,8 @@ void Engine::decrement_pending(Operation* op) {
       inline_ready_.push_back(op);
     } else {
       ready_.push_back(op);
-      work_cv_.notify_one();
+      ready_count_.fetch_add(1, std::memory_order_release);
+      if (sleepers_ > 0) work_cv_.notify_one();
     }
   }
 }
@@ -250,7 +261,14 @@ void Engine::complete(Operation* op, EventRef done, std::exception_ptr failure) 
     auto it = std::find_if(var.queue.begin(), var.queue.end(),
                            [op](const QueueEntry& e) { return e.op == op && !e.write; });
     var.queue.erase(it);
-    if (done) var.readers.push_back(done);
+    if (done) {
+      // events on one lane complete in order: keep only the newest per lane,
+      // so a tag that is read every step but rarely written stays O(lanes)
+      auto same = std::find_if(var.readers.begin(), var.readers.end(),
+                               [&](const EventRef& r) { return r->lane == done->lane; });
+      if (same != var.readers.end()) *same = done;
+      else var.readers.push_back(done);
+    }
     grant_head(var);
   }
   for (uint64_t t : op->mutates) {
@@ -371,22 +389,22 @@ void Engine::run_op(Operation* op) {
     try {
       bind_device();
       stream = lane_stream(op->lane);
-      const EventObj* seen[32];
-      int nseen = 0;
-      for (const EventRef& d : op->deps) {
-        if (d->lane == op->lane) continue;  // same stream: already ordered
-        bool dup = false;
-        for (int i = 0; i < nseen; ++i) dup = dup || seen[i] == d.get();
-        if (dup) continue;
-        if (nseen < 32) seen[nseen++] = d.get();
-        CSB_CUDA(cudaStreamWaitEvent(stream, d->ev, 0));
-      }
+      // one wait per distinct event; same-lane events are already ordered
+      std::vector<const EventObj*> waits;
+      waits.reserve(op->deps.size());
+      for (const EventRef& d : op->deps)
+        if (d->lane != op->lane) waits.push_back(d.get());
+      std::sort(waits.begin(), waits.end());
+      waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
+      hostprof::Scope prof(hostprof::kDispatchWait);
+      for (const EventObj* d : waits) CSB_CUDA(cudaStreamWaitEvent(stream, d->ev, 0));
     } catch (...) {
       failure = std::current_exception();
     }
     op->deps.clear();
     emit("op_started");
     if (!failure) {
+      hostprof::Scope prof(hostprof::kDispatchBody);
       try {
         op->stream_body(stream);
       } catch (...) {
@@ -394,6 +412,7 @@ void Engine::run_op(Operation* op) {
       }
     }
     try {
+      hostprof::Scope prof(hostprof::kDispatchRecord);
       if (stream) {
         done = acquire_event(op->lane);
         CSB_CUDA(cudaEventRecord(done->ev, stream));
@@ -404,6 +423,7 @@ void Engine::run_op(Operation* op) {
     }
     emit("op_finished");
   }
+  hostprof::Scope prof(hostprof::kComplete);
   std::lock_guard<std::mutex> lock(mu_);
   complete(op, std::move(done), failure);
 }
@@ -421,15 +441,30 @@ void Engine::drain_inline() {
   }
 }
 
+// Workers spin on the ready counter for a short while before blocking: a
+// blocked thread takes tens of microseconds to wake, and every DepCha /
+// ConCom collective is handed to the pool, so wake-up latency would
+// otherwise serialize into the step (CSB_ENGINE_SPIN_US, default 200).
 void Engine::worker_loop() {
   for (;;) {
+    const auto spin_until = std::chrono::steady_clock::now() + spin_;
+    while (ready_count_.load(std::memory_order_acquire) == 0 &&
+           !stop_flag_.load(std::memory_order_relaxed) &&
+           std::chrono::steady_clock::now() < spin_until) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    }
     Operation* op = nullptr;
     {
       std::unique_lock<std::mutex> lock(mu_);
+      ++sleepers_;
       work_cv_.wait(lock, [this] { return stopping_ || !ready_.empty(); });
+      --sleepers_;
       if (ready_.empty()) return;  // stopping and drained
       op = ready_.front();
       ready_.pop_front();
+      ready_count_.fetch_sub(1, std::memory_order_relaxed);
     }
     run_op(op);
     drain_inline();
@@ -468,19 +503,14 @@ void Engine::shutdown() {
     if (shut_down_) return;
     stopping_ = true;
     shut_down_ = true;
+    stop_flag_.store(true);
     work_cv_.notify_all();
   }
   for (std::thread& t : workers_) t.join();
 }
 
-uint64_t Engine::ops_pushed() const {
-  std::lock_guard<std::mutex> lock(mu_);
-  return next_op_;
-}
+uint64_t Engine::ops_pushed() const { return next_op_.load(std::memory_order_acquire); }
 
-uint64_t Engine::ops_completed() const {
-  std::lock_guard<std::mutex> lock(mu_);
-  return ops_done_;
-}
+uint64_t Engine::ops_completed() const { return ops_done_.load(std::memory_order_acquire); }
 
 }  // namespace csb

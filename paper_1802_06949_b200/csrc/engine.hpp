@@ -160,13 +160,17 @@ class Engine {
   std::deque<Operation*> inline_ready_;  // dispatched by the granting thread
   std::unordered_map<OpId, std::unique_ptr<Operation>> live_;
   uint64_t next_tag_ = 0;
-  OpId next_op_ = 0;
-  uint64_t ops_done_ = 0;
+  std::atomic<OpId> next_op_{0};      // written under mu_, read lock-free
+  std::atomic<uint64_t> ops_done_{0};  // written under mu_, read lock-free
   bool stopping_ = false;
   bool shut_down_ = false;
   bool poisoned_ = false;
   std::exception_ptr first_failure_;
   std::vector<std::thread> workers_;
+  std::atomic<int> ready_count_{0};
+  std::atomic<bool> stop_flag_{false};
+  int sleepers_ = 0;  // mu_
+  std::chrono::microseconds spin_{200};
 
   std::vector<cudaStream_t> lanes_;
   mutable std::mutex lanes_mu_;

@@ -11,14 +11,16 @@
 //   cs_checksum        : deterministic fp64 checksum (e2e result read-back)
 //
 // Design (B200, HBM-bound, no tensor cores):
-//   * 256-thread CTAs; every thread moves 8 elements per step as 16-byte
-//     vectors (ld/st .v4 / .v2.f64), 2 steps unrolled with all loads issued
-//     before any store -> 4096-element chunks, >= 64 B in flight per thread.
-//   * A launch covers a whole table of keys (one bucket): the per-entry
-//     chunk prefix sums, pointers and sizes travel in a __grid_constant__
-//     kernel-parameter block (<= 15 KB, constant bank), so no host->device
-//     copy precedes a launch; a CTA finds its entry by binary search.
-//   * Grid = min(chunks, 148 SMs x 8 resident CTAs), grid-stride over chunks.
+//   * 256-thread CTAs; a thread moves groups of 8 elements as 16-byte
+//     vectors (ld/st .v4 / .v2.f64), 2-4 groups unrolled with every load
+//     issued before the first store (>= 64 B in flight per thread).
+//   * A launch covers a whole table of keys (one bucket): per-entry group
+//     prefix sums, pointers and sizes travel in a __grid_constant__
+//     kernel-parameter block (<= 21 KB, constant bank), so no host->device
+//     copy precedes a launch; a CTA finds its first entry by binary search.
+//   * Grid = exactly one wave (148 SMs x occupancy of the instantiation);
+//     the table's groups are split evenly over it, so every CTA moves the
+//     same bytes and there is no tail wave.
 //   * Arithmetic uses explicit round-to-nearest intrinsics (__dmul_rn,
 //     __fsub_rn, ...) so nothing is contracted into an FMA: fp64 results are
 //     bit-identical to the reference, fp32 to the oracle's fp32 restatement.
@@ -26,20 +28,22 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "common.hpp"
+#include "hostprof.hpp"
+#include "kernels.hpp"
 
 namespace csb {
 namespace {
 
 constexpr int kThreads = 256;
 constexpr int kVec = 8;     // elements per thread per step
-constexpr int kUnroll = 2;  // steps in flight per thread
-constexpr int kChunk = kThreads * kVec * kUnroll;  // 4096 elements
 
 // ------------------------------------------------------------ vector IO
 
@@ -240,17 +244,28 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 
 // ------------------------------------------------------- table lookup
 
-template <int CAP>
-__device__ __forceinline__ int find_entry(const uint32_t* chunk_start, int n_entries, uint32_t c) {
-  // largest e with chunk_start[e] <= c  (chunk_start[0] = 0, strictly
-  // increasing over non-empty entries; empty entries are never produced)
+// Work is counted in GROUPS of kVec = 8 consecutive elements (one or more
+// 16-byte vectors).  A launch covers the concatenation of its table's
+// entries, T groups in total, split EVENLY over a single wave of CTAs
+// (grid = SMs x resident CTAs): CTA c owns groups [T*c/G, T*(c+1)/G), which
+// may span several entries.  Every CTA therefore moves the same number of
+// bytes and finishes together -- no wave-quantization tail, the dominant
+// loss of a chunk-per-CTA grid on buckets of a few thousand chunks.
+
+__device__ __forceinline__ int find_entry(const uint64_t* group_start, int n_entries, uint64_t g) {
+  // largest e with group_start[e] <= g (group_start[0] = 0; entries non-empty)
   int lo = 0, hi = n_entries - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
-    if (chunk_start[mid] <= c) lo = mid;
+    if (group_start[mid] <= g) lo = mid;
     else hi = mid - 1;
   }
   return lo;
+}
+
+__device__ __forceinline__ void cta_range(uint64_t T, uint64_t& g0, uint64_t& g1) {
+  g0 = T * blockIdx.x / gridDim.x;
+  g1 = T * (blockIdx.x + 1) / gridDim.x;
 }
 
 // ------------------------------------------------------------ (a) pack
@@ -258,44 +273,54 @@ __device__ __forceinline__ int find_entry(const uint32_t* chunk_start, int n_ent
 template <int CAP>
 struct PackParams {
   int n_entries;
-  uint32_t total_chunks;
-  uint32_t chunk_start[CAP];
+  uint64_t total_groups;
+  uint64_t group_start[CAP];
   const void* src[CAP];
   void* dst[CAP];
   uint64_t n[CAP];
   uint8_t vec_ok[CAP];
 };
 
+// groups [lo, hi) of one entry, all threads of the CTA
+template <int SDT, int DDT>
+__device__ __forceinline__ void pack_segment(const void* src, void* dst, uint64_t n, bool vec,
+                                             uint64_t lo, uint64_t hi) {
+  using Acc = typename AccOf<SDT, DDT>::T;
+  constexpr int U = 4;
+  uint64_t q = lo + threadIdx.x;
+  if (vec) {
+    const uint64_t hi_full = min(hi, n / kVec);  // groups with all 8 elements present
+    for (; q + (U - 1) * kThreads < hi_full; q += U * kThreads) {
+      Acc v[U][kVec];
+#pragma unroll
+      for (int u = 0; u < U; ++u) load8<SDT, Acc>(src, (q + u * kThreads) * kVec, v[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) store8<DDT, Acc>(dst, (q + u * kThreads) * kVec, v[u]);
+    }
+    for (; q < hi_full; q += kThreads) {
+      Acc v[kVec];
+      load8<SDT, Acc>(src, q * kVec, v);
+      store8<DDT, Acc>(dst, q * kVec, v);
+    }
+  }
+  for (; q < hi; q += kThreads) {
+    const uint64_t end = min(n, (q + 1) * kVec);
+    for (uint64_t j = q * kVec; j < end; ++j) store1<DDT, Acc>(dst, j, load1<SDT, Acc>(src, j));
+  }
+}
+
 template <int SDT, int DDT, int CAP>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackParams<CAP> p) {
-  using Acc = typename AccOf<SDT, DDT>::T;
-  for (uint32_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
-    const int e = find_entry<CAP>(p.chunk_start, p.n_entries, c);
-    const uint64_t base = static_cast<uint64_t>(c - p.chunk_start[e]) * kChunk;
-    const uint64_t n = p.n[e];
-    const uint64_t end = min(n, base + kChunk);
-    const void* src = p.src[e];
-    void* dst = p.dst[e];
-    if (p.vec_ok[e]) {
-      Acc v[kUnroll][kVec];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t i = base + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * kVec;
-        if (i + kVec <= end) load8<SDT, Acc>(src, i, v[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t i = base + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * kVec;
-        if (i + kVec <= end) {
-          store8<DDT, Acc>(dst, i, v[u]);
-        } else {
-          for (uint64_t j = i; j < end; ++j) store1<DDT, Acc>(dst, j, load1<SDT, Acc>(src, j));
-        }
-      }
-    } else {
-      for (uint64_t j = base + threadIdx.x; j < end; j += kThreads)
-        store1<DDT, Acc>(dst, j, load1<SDT, Acc>(src, j));
-    }
+  uint64_t g0, g1;
+  cta_range(p.total_groups, g0, g1);
+  if (g0 >= g1) return;
+  int e = find_entry(p.group_start, p.n_entries, g0);
+  for (uint64_t g = g0; g < g1; ++e) {
+    const uint64_t es = p.group_start[e];
+    const uint64_t ee = (e + 1 < p.n_entries) ? p.group_start[e + 1] : p.total_groups;
+    const uint64_t hi = min(g1, ee);
+    pack_segment<SDT, DDT>(p.src[e], p.dst[e], p.n[e], p.vec_ok[e], g - es, hi - es);
+    g = hi;
   }
 }
 
@@ -307,47 +332,53 @@ struct SumParams {
   int m;
   int nout;
   uint64_t n;
-  uint32_t total_chunks;
+  uint64_t total_groups;
   int vec_ok;
 };
 
+// fixed rank order: ((b0 + b1) + b2) + ...  (collective.cpp:229-233); all M
+// inputs of a group are loaded before the first add, so a thread keeps M
+// 16-byte loads in flight (local or NVLink peer addresses alike).
 template <int DT, int M>
 __global__ void __launch_bounds__(kThreads) sum_kernel(const __grid_constant__ SumParams p) {
   using Acc = typename AccOf<DT, DT>::T;  // f64 -> f64, f32 -> f32, bf16 -> f32
   const int m = (M > 0) ? M : p.m;
-  for (uint32_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
-    const uint64_t base = static_cast<uint64_t>(c) * kChunk;
-    const uint64_t end = min(p.n, base + kChunk);
-    if (p.vec_ok) {
+  uint64_t g0, g1;
+  cta_range(p.total_groups, g0, g1);
+  uint64_t q = g0 + threadIdx.x;
+  if (p.vec_ok) {
+    const uint64_t hi_full = min(g1, p.n / kVec);
+    for (; q < hi_full; q += kThreads) {
+      const uint64_t i = q * kVec;
+      Acc acc[kVec];
+      if constexpr (M > 0) {
+        Acc x[M][kVec];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t i = base + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * kVec;
-        if (i + kVec <= end) {
-          Acc acc[kVec];
-          load8_rw<DT, Acc>(p.in[0], i, acc);
-          // fixed rank order: ((b0 + b1) + b2) + ...  (collective.cpp:229-233)
-#pragma unroll 4
-          for (int r = 1; r < m; ++r) {
-            Acc x[kVec];
-            load8_rw<DT, Acc>(p.in[r], i, x);
+        for (int r = 0; r < M; ++r) load8_rw<DT, Acc>(p.in[r], i, x[r]);
 #pragma unroll
-            for (int q = 0; q < kVec; ++q) acc[q] = add_rn(acc[q], x[q]);
-          }
-          for (int o = 0; o < p.nout; ++o) store8<DT, Acc>(p.out[o], i, acc);
-        } else if (i < end) {
-          for (uint64_t j = i; j < end; ++j) {
-            Acc a = load1<DT, Acc>(p.in[0], j);
-            for (int r = 1; r < m; ++r) a = add_rn(a, load1<DT, Acc>(p.in[r], j));
-            for (int o = 0; o < p.nout; ++o) store1<DT, Acc>(p.out[o], j, a);
-          }
+        for (int j = 0; j < kVec; ++j) acc[j] = x[0][j];
+#pragma unroll
+        for (int r = 1; r < M; ++r)
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[r][j]);
+      } else {
+        load8_rw<DT, Acc>(p.in[0], i, acc);
+        for (int r = 1; r < m; ++r) {
+          Acc x[kVec];
+          load8_rw<DT, Acc>(p.in[r], i, x);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[j]);
         }
       }
-    } else {
-      for (uint64_t j = base + threadIdx.x; j < end; j += kThreads) {
-        Acc a = load1<DT, Acc>(p.in[0], j);
-        for (int r = 1; r < m; ++r) a = add_rn(a, load1<DT, Acc>(p.in[r], j));
-        for (int o = 0; o < p.nout; ++o) store1<DT, Acc>(p.out[o], j, a);
-      }
+      for (int o = 0; o < p.nout; ++o) store8<DT, Acc>(p.out[o], i, acc);
+    }
+  }
+  for (; q < g1; q += kThreads) {
+    const uint64_t end = min(p.n, (q + 1) * kVec);
+    for (uint64_t j = q * kVec; j < end; ++j) {
+      Acc a = load1<DT, Acc>(p.in[0], j);
+      for (int r = 1; r < m; ++r) a = add_rn(a, load1<DT, Acc>(p.in[r], j));
+      for (int o = 0; o < p.nout; ++o) store1<DT, Acc>(p.out[o], j, a);
     }
   }
 }
@@ -357,10 +388,10 @@ __global__ void __launch_bounds__(kThreads) sum_kernel(const __grid_constant__ S
 template <int CAP>
 struct SgdParams {
   int n_entries;
-  uint32_t total_chunks;
+  uint64_t total_groups;
   double step;  // lr * rescale, computed in fp64 exactly as model.cpp:21
   double mu;
-  uint32_t chunk_start[CAP];
+  uint64_t group_start[CAP];
   void* w[CAP];
   const void* g[CAP];
   void* mom[CAP];
@@ -368,73 +399,121 @@ struct SgdParams {
   uint8_t vec_ok[CAP];
 };
 
-template <int WDT, int GDT, bool MOM, int CAP>
-__global__ void __launch_bounds__(kThreads) sgd_kernel(const __grid_constant__ SgdParams<CAP> p) {
+template <bool MOM, typename Acc>
+__device__ __forceinline__ void sgd_elem(Acc& w, Acc g, Acc& m, Acc step, Acc mu) {
+  if constexpr (MOM) {
+    const Acc v = sub_rn(mul_rn(mu, m), mul_rn(step, g));  // v = mu*v - step*g
+    m = v;
+    w = add_rn(w, v);                                      // w = w + v
+  } else {
+    w = sub_rn(w, mul_rn(step, g));                        // w -= step*g (model.cpp:25)
+  }
+}
+
+template <int WDT, int GDT, bool MOM>
+__device__ __forceinline__ void sgd_segment(void* w, const void* g, void* mom, uint64_t n, bool vec,
+                                            uint64_t lo, uint64_t hi, double step_d, double mu_d) {
   using Acc = typename AccOf<WDT, WDT>::T;  // f64 weights -> f64 math, else f32
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
-  const Acc step = static_cast<Acc>(p.step);
-  const Acc mu = static_cast<Acc>(p.mu);
-  for (uint32_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
-    const int e = find_entry<CAP>(p.chunk_start, p.n_entries, c);
-    const uint64_t base = static_cast<uint64_t>(c - p.chunk_start[e]) * kChunk;
-    const uint64_t end = min(p.n[e], base + kChunk);
-    void* w = p.w[e];
-    const void* g = p.g[e];
-    void* mom = p.mom[e];
-    if (p.vec_ok[e]) {
-      Acc gv[kUnroll][kVec], wv[kUnroll][kVec], mv[kUnroll][kVec];
+  constexpr int U = 2;
+  const Acc step = static_cast<Acc>(step_d);
+  const Acc mu = static_cast<Acc>(mu_d);
+  uint64_t q = lo + threadIdx.x;
+  if (vec) {
+    const uint64_t hi_full = min(hi, n / kVec);
+    for (; q + (U - 1) * kThreads < hi_full; q += U * kThreads) {
+      Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t i = base + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * kVec;
-        if (i + kVec <= end) {
-          load8<GDT, Acc>(g, i, gv[u]);
-          load8_rw<WDT, Acc>(w, i, wv[u]);
-          if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv[u]);
-        }
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = (q + u * kThreads) * kVec;
+        load8<GDT, Acc>(g, i, gv[u]);
+        load8_rw<WDT, Acc>(w, i, wv[u]);
+        if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv[u]);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint64_t i = base + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * kVec;
-        if (i + kVec <= end) {
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = (q + u * kThreads) * kVec;
 #pragma unroll
-          for (int q = 0; q < kVec; ++q) {
-            if constexpr (MOM) {
-              const Acc v = sub_rn(mul_rn(mu, mv[u][q]), mul_rn(step, gv[u][q]));
-              mv[u][q] = v;
-              wv[u][q] = add_rn(wv[u][q], v);
-            } else {
-              wv[u][q] = sub_rn(wv[u][q], mul_rn(step, gv[u][q]));
-            }
-          }
-          store8<WDT, Acc>(w, i, wv[u]);
-          if constexpr (MOM) store8<MDT, Acc>(mom, i, mv[u]);
-        } else {
-          for (uint64_t j = i; j < end; ++j) {
-            Acc gg = load1<GDT, Acc>(g, j), ww = load1<WDT, Acc>(w, j);
-            if constexpr (MOM) {
-              const Acc v = sub_rn(mul_rn(mu, load1<MDT, Acc>(mom, j)), mul_rn(step, gg));
-              store1<MDT, Acc>(mom, j, v);
-              ww = add_rn(ww, v);
-            } else {
-              ww = sub_rn(ww, mul_rn(step, gg));
-            }
-            store1<WDT, Acc>(w, j, ww);
-          }
-        }
-      }
-    } else {
-      for (uint64_t j = base + threadIdx.x; j < end; j += kThreads) {
-        Acc gg = load1<GDT, Acc>(g, j), ww = load1<WDT, Acc>(w, j);
-        if constexpr (MOM) {
-          const Acc v = sub_rn(mul_rn(mu, load1<MDT, Acc>(mom, j)), mul_rn(step, gg));
-          store1<MDT, Acc>(mom, j, v);
-          ww = add_rn(ww, v);
-        } else {
-          ww = sub_rn(ww, mul_rn(step, gg));
-        }
-        store1<WDT, Acc>(w, j, ww);
+        for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[u][j], gv[u][j], mv[u][j], step, mu);
+        store8<WDT, Acc>(w, i, wv[u]);
+        if constexpr (MOM) store8<MDT, Acc>(mom, i, mv[u]);
       }
     }
+    for (; q < hi_full; q += kThreads) {
+      const uint64_t i = q * kVec;
+      Acc gv[kVec], wv[kVec], mv[kVec];
+      load8<GDT, Acc>(g, i, gv);
+      load8_rw<WDT, Acc>(w, i, wv);
+      if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[j], gv[j], mv[j], step, mu);
+      store8<WDT, Acc>(w, i, wv);
+      if constexpr (MOM) store8<MDT, Acc>(mom, i, mv);
+    }
+  }
+  for (; q < hi; q += kThreads) {
+    const uint64_t end = min(n, (q + 1) * kVec);
+    for (uint64_t j = q * kVec; j < end; ++j) {
+      Acc ww = load1<WDT, Acc>(w, j), mm = Acc(0);
+      if constexpr (MOM) mm = load1<MDT, Acc>(mom, j);
+      sgd_elem<MOM>(ww, load1<GDT, Acc>(g, j), mm, step, mu);
+      if constexpr (MOM) store1<MDT, Acc>(mom, j, mm);
+      store1<WDT, Acc>(w, j, ww);
+    }
+  }
+}
+
+template <int WDT, int GDT, bool MOM, int CAP>
+__global__ void __launch_bounds__(kThreads) sgd_kernel(const __grid_constant__ SgdParams<CAP> p) {
+  uint64_t g0, g1;
+  cta_range(p.total_groups, g0, g1);
+  if (g0 >= g1) return;
+  int e = find_entry(p.group_start, p.n_entries, g0);
+  for (uint64_t g = g0; g < g1; ++e) {
+    const uint64_t es = p.group_start[e];
+    const uint64_t ee = (e + 1 < p.n_entries) ? p.group_start[e + 1] : p.total_groups;
+    const uint64_t hi = min(g1, ee);
+    sgd_segment<WDT, GDT, MOM>(p.w[e], p.g[e], p.mom[e], p.n[e], p.vec_ok[e], g - es, hi - es,
+                               p.step, p.mu);
+    g = hi;
+  }
+}
+
+// ------------------------------------ device-resident tables (buckets)
+
+using DevEntry = DeviceTable::Entry;
+
+// Same even split as the parameter-block kernels; the CTA's first entry was
+// precomputed on the host, so a CTA starts with one dependent L2 load
+// instead of a binary search, and entries are read through L1 (broadcast).
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kThreads)
+    pack_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
+                    const uint8_t* __restrict__ vec, uint64_t total) {
+  uint64_t g0, g1;
+  cta_range(total, g0, g1);
+  if (g0 >= g1) return;
+  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
+    const DevEntry en = tab[e];
+    const uint64_t hi = min(g1, en.gend);
+    pack_segment<SDT, DDT>(en.a, en.c, en.n, vec[e], g0 - en.gstart, hi - en.gstart);
+    g0 = hi;
+  }
+}
+
+template <int WDT, int GDT, bool MOM>
+__global__ void __launch_bounds__(kThreads)
+    sgd_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
+                   const uint8_t* __restrict__ vec, uint64_t total, double step, double mu) {
+  uint64_t g0, g1;
+  cta_range(total, g0, g1);
+  if (g0 >= g1) return;
+  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
+    const DevEntry en = tab[e];
+    const uint64_t hi = min(g1, en.gend);
+    sgd_segment<WDT, GDT, MOM>(en.c, en.a, const_cast<void*>(en.b), en.n, vec[e], g0 - en.gstart,
+                               hi - en.gstart, step, mu);
+    g0 = hi;
   }
 }
 
@@ -495,6 +574,64 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const void* x, uint6
 
 // ------------------------------------------------------------ host side
 
+// Launch counter (always on) and per-launch event timing (profiling on).
+std::atomic<uint64_t> g_launches{0};
+std::atomic<bool> g_prof_on{false};
+struct ProfRec {
+  int kind;
+  int dev;
+  cudaEvent_t a, b;
+  double bytes;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_pending;
+std::vector<std::pair<int, cudaEvent_t>> g_prof_free;
+KernelStats g_prof_stats[kKernKinds];
+uint64_t g_launch_kind[kKernKinds];
+
+cudaEvent_t prof_event(int dev) {
+  {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    for (size_t i = 0; i < g_prof_free.size(); ++i) {
+      if (g_prof_free[i].first == dev) {
+        cudaEvent_t e = g_prof_free[i].second;
+        g_prof_free.erase(g_prof_free.begin() + static_cast<long>(i));
+        return e;
+      }
+    }
+  }
+  cudaEvent_t e;
+  CSB_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// Brackets one launch: counts it, and when profiling is on records a pair
+// of timing events on the launch stream (the kernel's own stream).
+struct LaunchScope {
+  int kind;
+  double bytes;
+  cudaStream_t s;
+  int dev = -1;
+  cudaEvent_t a = nullptr, b = nullptr;
+  hostprof::Scope prof{hostprof::kLaunch};
+  LaunchScope(int k, double by, cudaStream_t st) : kind(k), bytes(by), s(st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (g_prof_on.load(std::memory_order_relaxed)) {
+      CSB_CUDA(cudaGetDevice(&dev));
+      a = prof_event(dev);
+      b = prof_event(dev);
+      CSB_CUDA(cudaEventRecord(a, s));
+    }
+  }
+  void done() {
+    if (!a) return;
+    CSB_CUDA(cudaEventRecord(b, s));
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    g_prof_pending.push_back(ProfRec{kind, dev, a, b, bytes});
+    g_launch_kind[kind]++;
+  }
+};
+
 int sm_count_for_current_device() {
   static std::mutex mu;
   static std::vector<int> cache;
@@ -510,10 +647,21 @@ int sm_count_for_current_device() {
   return cache[dev];
 }
 
-inline int grid_for(uint32_t chunks) {
-  const int cap = sm_count_for_current_device() * (2048 / kThreads);
-  return static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(chunks, cap)));
+// One full wave: SMs x resident CTAs of this kernel (occupancy queried once
+// per instantiation), fewer when there is less than a group per thread.
+template <typename Kernel>
+int wave_grid(Kernel kernel, uint64_t groups) {
+  static const int occ = [&] {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess) b = 1;
+    return std::max(1, b);
+  }();
+  const uint64_t full = static_cast<uint64_t>(sm_count_for_current_device()) * occ;
+  const uint64_t need = (groups + kThreads - 1) / kThreads;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
 }
+
+inline uint64_t groups_of(uint64_t n) { return (n + kVec - 1) / kVec; }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -527,29 +675,31 @@ void launch_pack_cap(const cs_copy_entry* es, int n, int sdt, int ddt, cudaStrea
 
 template <int SDT, int DDT, int CAP>
 void launch_pack_typed(const PackParams<CAP>& p, cudaStream_t s) {
-  pack_kernel<SDT, DDT, CAP><<<grid_for(p.total_chunks), kThreads, 0, s>>>(p);
+  double elems = 0;
+  for (int i = 0; i < p.n_entries; ++i) elems += static_cast<double>(p.n[i]);
+  LaunchScope ls(kKernPack, elems * (sizeof(typename Elem<SDT>::T) + sizeof(typename Elem<DDT>::T)), s);
+  pack_kernel<SDT, DDT, CAP><<<wave_grid(pack_kernel<SDT, DDT, CAP>, p.total_groups), kThreads, 0, s>>>(p);
   check_launch("pack_kernel");
+  ls.done();
 }
 
 template <int CAP>
 void launch_pack_cap(const cs_copy_entry* es, int n, int sdt, int ddt, cudaStream_t s) {
   PackParams<CAP> p;
   p.n_entries = 0;
-  uint32_t chunks = 0;
+  uint64_t groups = 0;
   for (int i = 0; i < n; ++i) {
     if (es[i].n == 0) continue;
     if (!es[i].src || !es[i].dst) throw UsageError("cs_pack: null pointer in entry");
     const int k = p.n_entries++;
-    p.chunk_start[k] = chunks;
+    p.group_start[k] = groups;
     p.src[k] = es[i].src;
     p.dst[k] = es[i].dst;
     p.n[k] = es[i].n;
     p.vec_ok[k] = aligned16(es[i].src) && aligned16(es[i].dst);
-    const uint64_t c = (es[i].n + kChunk - 1) / kChunk;
-    if (chunks + c > 0xFFFFFFF0ull) throw UsageError("cs_pack: table too large");
-    chunks += static_cast<uint32_t>(c);
+    groups += groups_of(es[i].n);
   }
-  p.total_chunks = chunks;
+  p.total_groups = groups;
   if (p.n_entries == 0) return;
 #define CSB_PACK_CASE(S, D) \
   if (sdt == S && ddt == D) return launch_pack_typed<S, D, CAP>(p, s);
@@ -568,8 +718,14 @@ void launch_pack_cap(const cs_copy_entry* es, int n, int sdt, int ddt, cudaStrea
 
 template <int WDT, int GDT, bool MOM, int CAP>
 void launch_sgd_typed(const SgdParams<CAP>& p, cudaStream_t s) {
-  sgd_kernel<WDT, GDT, MOM, CAP><<<grid_for(p.total_chunks), kThreads, 0, s>>>(p);
+  double elems = 0;
+  for (int i = 0; i < p.n_entries; ++i) elems += static_cast<double>(p.n[i]);
+  const double mom_bytes = MOM ? 2.0 * (WDT == CS_F64 ? 8 : 4) : 0.0;
+  LaunchScope ls(kKernSgd,
+                 elems * (2.0 * sizeof(typename Elem<WDT>::T) + sizeof(typename Elem<GDT>::T) + mom_bytes), s);
+  sgd_kernel<WDT, GDT, MOM, CAP><<<wave_grid(sgd_kernel<WDT, GDT, MOM, CAP>, p.total_groups), kThreads, 0, s>>>(p);
   check_launch("sgd_kernel");
+  ls.done();
 }
 
 template <int CAP>
@@ -580,21 +736,21 @@ void launch_sgd_cap(const cs_update_entry* es, int n, int wdt, int gdt, double l
   p.step = lr * rescale;  // model.cpp:21, fp64 on the host
   p.mu = momentum;
   const bool mom = momentum != 0.0;
-  uint32_t chunks = 0;
+  uint64_t groups = 0;
   for (int i = 0; i < n; ++i) {
     if (es[i].n == 0) continue;
     if (!es[i].w || !es[i].g) throw UsageError("cs_sgd_update: null pointer in entry");
     if (mom && !es[i].mom) throw UsageError("cs_sgd_update: momentum > 0 needs a momentum buffer");
     const int k = p.n_entries++;
-    p.chunk_start[k] = chunks;
+    p.group_start[k] = groups;
     p.w[k] = es[i].w;
     p.g[k] = es[i].g;
     p.mom[k] = es[i].mom;
     p.n[k] = es[i].n;
     p.vec_ok[k] = aligned16(es[i].w) && aligned16(es[i].g) && (!mom || aligned16(es[i].mom));
-    chunks += static_cast<uint32_t>((es[i].n + kChunk - 1) / kChunk);
+    groups += groups_of(es[i].n);
   }
-  p.total_chunks = chunks;
+  p.total_groups = groups;
   if (p.n_entries == 0) return;
 #define CSB_SGD_CASE(W, G)                                                  \
   if (wdt == W && gdt == G) {                                               \
@@ -660,16 +816,19 @@ void sum_buffers(const void* const* in, int m, void* const* out, int nout, uint6
   p.m = m;
   p.nout = nout;
   p.n = n;
-  p.total_chunks = static_cast<uint32_t>((n + kChunk - 1) / kChunk);
+  p.total_groups = groups_of(n);
   p.vec_ok = vec ? 1 : 0;
-  const int grid = grid_for(p.total_chunks);
-#define CSB_SUM_M(DT)                                                                   \
-  switch (m) {                                                                          \
-    case 1: sum_kernel<DT, 1><<<grid, kThreads, 0, s>>>(p); break;                      \
-    case 2: sum_kernel<DT, 2><<<grid, kThreads, 0, s>>>(p); break;                      \
-    case 4: sum_kernel<DT, 4><<<grid, kThreads, 0, s>>>(p); break;                      \
-    case 8: sum_kernel<DT, 8><<<grid, kThreads, 0, s>>>(p); break;                      \
-    default: sum_kernel<DT, 0><<<grid, kThreads, 0, s>>>(p); break;                     \
+  LaunchScope ls(kKernSum, static_cast<double>(n) * dtype_size(dt) * (m + nout), s);
+#define CSB_SUM_LAUNCH(DT, M) \
+  sum_kernel<DT, M><<<wave_grid(sum_kernel<DT, M>, p.total_groups), kThreads, 0, s>>>(p)
+#define CSB_SUM_M(DT)                          \
+  switch (m) {                                 \
+    case 1: CSB_SUM_LAUNCH(DT, 1); break;      \
+    case 2: CSB_SUM_LAUNCH(DT, 2); break;      \
+    case 3: CSB_SUM_LAUNCH(DT, 3); break;      \
+    case 4: CSB_SUM_LAUNCH(DT, 4); break;      \
+    case 8: CSB_SUM_LAUNCH(DT, 8); break;      \
+    default: CSB_SUM_LAUNCH(DT, 0); break;     \
   }
   switch (dt) {
     case CS_F64: CSB_SUM_M(CS_F64); break;
@@ -678,12 +837,15 @@ void sum_buffers(const void* const* in, int m, void* const* out, int nout, uint6
     default: throw UsageError("cs_sum_buffers: unknown dtype");
   }
 #undef CSB_SUM_M
+#undef CSB_SUM_LAUNCH
   check_launch("sum_kernel");
+  ls.done();
 }
 
 void synth_backward(const void* src, void* dst, uint64_t n, int dt, uint64_t spin_ns, int ctas,
                     cudaStream_t s) {
   const int grid = ctas > 0 ? ctas : sm_count_for_current_device();
+  LaunchScope ls(kKernSynth, static_cast<double>(n) * 2 * (n ? dtype_size(dt) : 0), s);
   switch (dt) {
     case CS_F64: synth_backward_kernel<CS_F64><<<grid, kThreads, 0, s>>>(src, dst, n, spin_ns); break;
     case CS_F32: synth_backward_kernel<CS_F32><<<grid, kThreads, 0, s>>>(src, dst, n, spin_ns); break;
@@ -691,6 +853,7 @@ void synth_backward(const void* src, void* dst, uint64_t n, int dt, uint64_t spi
     default: throw UsageError("cs_synth_backward: unknown dtype");
   }
   check_launch("synth_backward_kernel");
+  ls.done();
 }
 
 namespace {
@@ -716,6 +879,7 @@ void checksum(const void* x, uint64_t n, int dt, double* out, cudaStream_t s) {
     }
     sc = per_dev[dev];
   }
+  LaunchScope ls(kKernChecksum, static_cast<double>(n) * dtype_size(dt), s);
   switch (dt) {
     case CS_F64: checksum_kernel<CS_F64><<<kSumBlocks, kThreads, 0, s>>>(x, n, sc.partial, sc.counter, out); break;
     case CS_F32: checksum_kernel<CS_F32><<<kSumBlocks, kThreads, 0, s>>>(x, n, sc.partial, sc.counter, out); break;
@@ -723,6 +887,181 @@ void checksum(const void* x, uint64_t n, int dt, double* out, cudaStream_t s) {
     default: throw UsageError("cs_checksum: unknown dtype");
   }
   check_launch("checksum_kernel");
+  ls.done();
+}
+
+// ------------------------------------------------------- DeviceTable
+
+DeviceTable::~DeviceTable() {
+  if (dev_) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev_device_);
+    cudaFree(dev_);
+    cudaSetDevice(prev);
+  }
+}
+
+// Computes every CTA's first entry for the kernel's one-wave grid and makes
+// the device copy current (uploading only when the bytes differ).
+void DeviceTable::sync(const void* kernel_fn, cudaStream_t s) {
+  (void)kernel_fn;
+  first_.assign(static_cast<size_t>(grid_), 0);
+  size_t e = 0;
+  for (int c = 0; c < grid_; ++c) {
+    const uint64_t g0 = groups_ * static_cast<uint64_t>(c) / static_cast<uint64_t>(grid_);
+    while (e + 1 < host_.size() && host_[e].gend <= g0) ++e;
+    first_[static_cast<size_t>(c)] = static_cast<uint32_t>(e);
+  }
+  const size_t eb = host_.size() * sizeof(Entry), fb = first_.size() * 4, vb = vec_.size();
+  std::vector<unsigned char> img(eb + fb + vb);
+  std::memcpy(img.data(), host_.data(), eb);
+  std::memcpy(img.data() + eb, first_.data(), fb);
+  std::memcpy(img.data() + eb + fb, vec_.data(), vb);
+  int dev = 0;
+  CSB_CUDA(cudaGetDevice(&dev));
+  if (dev_ && dev == dev_device_ && img == shadow_) return;
+  void* fresh = nullptr;
+  CSB_CUDA(cudaMallocAsync(&fresh, img.size(), s));
+  // pageable source: staged before the call returns, ordered on `s`
+  CSB_CUDA(cudaMemcpyAsync(fresh, img.data(), img.size(), cudaMemcpyHostToDevice, s));
+  if (dev_) {
+    if (dev == dev_device_) CSB_CUDA(cudaFreeAsync(dev_, s));
+    else throw UsageError("DeviceTable: used from a different device");
+  }
+  dev_ = fresh;
+  dev_device_ = dev;
+  shadow_.swap(img);
+  ++uploads_;
+}
+
+void DeviceTable::pack(const cs_copy_entry* es, int n, int sdt, int ddt, cudaStream_t s) {
+  host_.clear();
+  vec_.clear();
+  groups_ = 0;
+  double elems = 0;
+  for (int i = 0; i < n; ++i) {
+    if (es[i].n == 0) continue;
+    if (!es[i].src || !es[i].dst) throw UsageError("cs_pack: null pointer in entry");
+    const uint64_t g = groups_of(es[i].n);
+    host_.push_back(Entry{es[i].src, nullptr, es[i].dst, es[i].n, groups_, groups_ + g});
+    vec_.push_back(aligned16(es[i].src) && aligned16(es[i].dst));
+    groups_ += g;
+    elems += static_cast<double>(es[i].n);
+  }
+  if (host_.empty()) return;
+  LaunchScope ls(kKernPack, elems * static_cast<double>(dtype_size(sdt) + dtype_size(ddt)), s);
+#define CSB_PACK_TAB(S, D)                                                              \
+  if (sdt == S && ddt == D) {                                                           \
+    grid_ = wave_grid(pack_tab_kernel<S, D>, groups_);                                  \
+    sync(reinterpret_cast<const void*>(pack_tab_kernel<S, D>), s);                      \
+    const char* base = static_cast<const char*>(dev_);                                  \
+    pack_tab_kernel<S, D><<<grid_, kThreads, 0, s>>>(                                   \
+        reinterpret_cast<const Entry*>(base),                                           \
+        reinterpret_cast<const uint32_t*>(base + host_.size() * sizeof(Entry)),         \
+        reinterpret_cast<const uint8_t*>(base + host_.size() * sizeof(Entry) + first_.size() * 4), \
+        groups_);                                                                       \
+    check_launch("pack_tab_kernel");                                                    \
+    ls.done();                                                                          \
+    return;                                                                             \
+  }
+  CSB_PACK_TAB(CS_F64, CS_F64)
+  CSB_PACK_TAB(CS_F32, CS_F32)
+  CSB_PACK_TAB(CS_F32, CS_BF16)
+  CSB_PACK_TAB(CS_BF16, CS_F32)
+  CSB_PACK_TAB(CS_BF16, CS_BF16)
+  CSB_PACK_TAB(CS_F32, CS_F64)
+  CSB_PACK_TAB(CS_F64, CS_F32)
+  CSB_PACK_TAB(CS_BF16, CS_F64)
+  CSB_PACK_TAB(CS_F64, CS_BF16)
+#undef CSB_PACK_TAB
+  throw UsageError("cs_pack: unsupported dtype pair");
+}
+
+void DeviceTable::sgd(const cs_update_entry* es, int n, int wdt, int gdt, double lr, double rescale,
+                      double momentum, cudaStream_t s) {
+  host_.clear();
+  vec_.clear();
+  groups_ = 0;
+  const bool mom = momentum != 0.0;
+  double elems = 0;
+  for (int i = 0; i < n; ++i) {
+    if (es[i].n == 0) continue;
+    if (!es[i].w || !es[i].g) throw UsageError("cs_sgd_update: null pointer in entry");
+    if (mom && !es[i].mom) throw UsageError("cs_sgd_update: momentum > 0 needs a momentum buffer");
+    const uint64_t g = groups_of(es[i].n);
+    host_.push_back(Entry{es[i].g, es[i].mom, es[i].w, es[i].n, groups_, groups_ + g});
+    vec_.push_back(aligned16(es[i].w) && aligned16(es[i].g) && (!mom || aligned16(es[i].mom)));
+    groups_ += g;
+    elems += static_cast<double>(es[i].n);
+  }
+  if (host_.empty()) return;
+  const double step = lr * rescale;  // model.cpp:21, fp64 on the host
+  const double mom_bytes = mom ? 2.0 * (wdt == CS_F64 ? 8 : 4) : 0.0;
+  LaunchScope ls(kKernSgd, elems * (2.0 * dtype_size(wdt) + dtype_size(gdt) + mom_bytes), s);
+#define CSB_SGD_TAB(W, G, M)                                                            \
+  if (wdt == W && gdt == G && mom == M) {                                               \
+    grid_ = wave_grid(sgd_tab_kernel<W, G, M>, groups_);                                \
+    sync(reinterpret_cast<const void*>(sgd_tab_kernel<W, G, M>), s);                    \
+    const char* base = static_cast<const char*>(dev_);                                  \
+    sgd_tab_kernel<W, G, M><<<grid_, kThreads, 0, s>>>(                                 \
+        reinterpret_cast<const Entry*>(base),                                           \
+        reinterpret_cast<const uint32_t*>(base + host_.size() * sizeof(Entry)),         \
+        reinterpret_cast<const uint8_t*>(base + host_.size() * sizeof(Entry) + first_.size() * 4), \
+        groups_, step, momentum);                                                       \
+    check_launch("sgd_tab_kernel");                                                     \
+    ls.done();                                                                          \
+    return;                                                                             \
+  }
+  CSB_SGD_TAB(CS_F64, CS_F64, false)
+  CSB_SGD_TAB(CS_F64, CS_F64, true)
+  CSB_SGD_TAB(CS_F32, CS_F32, false)
+  CSB_SGD_TAB(CS_F32, CS_F32, true)
+  CSB_SGD_TAB(CS_F32, CS_BF16, false)
+  CSB_SGD_TAB(CS_F32, CS_BF16, true)
+  CSB_SGD_TAB(CS_BF16, CS_BF16, false)
+  CSB_SGD_TAB(CS_BF16, CS_BF16, true)
+  CSB_SGD_TAB(CS_BF16, CS_F32, false)
+  CSB_SGD_TAB(CS_BF16, CS_F32, true)
+#undef CSB_SGD_TAB
+  throw UsageError(std::string("cs_sgd_update: unsupported dtype pair w=") + dtype_name(wdt) +
+                   " g=" + dtype_name(gdt));
+}
+
+uint64_t launch_count() { return g_launches.load(); }
+
+void profile_enable(bool on) { g_prof_on.store(on); }
+
+KernelStats profile_collect(int kind) {
+  if (kind < 0 || kind >= kKernKinds) throw UsageError("profile: unknown kernel kind");
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    recs.swap(g_prof_pending);
+  }
+  int prev = 0;
+  CSB_CUDA(cudaGetDevice(&prev));
+  for (const ProfRec& r : recs) {
+    CSB_CUDA(cudaSetDevice(r.dev));
+    CSB_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CSB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    g_prof_stats[r.kind].launches++;
+    g_prof_stats[r.kind].total_ms += ms;
+    g_prof_stats[r.kind].bytes += r.bytes;
+    g_prof_free.push_back({r.dev, r.a});
+    g_prof_free.push_back({r.dev, r.b});
+  }
+  CSB_CUDA(cudaSetDevice(prev));
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  return g_prof_stats[kind];
+}
+
+void profile_reset() {
+  profile_collect(0);
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  for (auto& s : g_prof_stats) s = KernelStats{};
 }
 
 }  // namespace csb

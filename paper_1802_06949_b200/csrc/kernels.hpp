@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "collsim_b200.h"
 
@@ -17,5 +18,55 @@ void sgd_update(const cs_update_entry* entries, int n, int w_dt, int g_dt, doubl
 void synth_backward(const void* src, void* dst, uint64_t n, int dt, uint64_t spin_ns, int ctas,
                     cudaStream_t s);
 void checksum(const void* x, uint64_t n, int dt, double* out, cudaStream_t s);
+
+// A kernel table kept resident in HBM for repeated launches over the same
+// keys (a KvStore bucket): the launch passes a pointer instead of a
+// parameter block of up to 21 KB, and the table is re-uploaded only when an
+// entry changes (stream-ordered cudaMallocAsync / copy / cudaFreeAsync, so
+// earlier launches on the same stream keep reading the old copy).  Every
+// launch through one DeviceTable must use the same stream.
+class DeviceTable {
+ public:
+  DeviceTable() = default;
+  ~DeviceTable();
+  DeviceTable(const DeviceTable&) = delete;
+  DeviceTable& operator=(const DeviceTable&) = delete;
+  void pack(const cs_copy_entry* es, int n, int src_dt, int dst_dt, cudaStream_t s);
+  void sgd(const cs_update_entry* es, int n, int w_dt, int g_dt, double lr, double rescale,
+           double momentum, cudaStream_t s);
+  uint64_t uploads() const { return uploads_; }
+
+  struct Entry {  // 48 B; a/b/c per kernel: pack a=src c=dst; sgd a=g b=mom c=w
+    const void* a;
+    const void* b;
+    void* c;
+    uint64_t n;
+    uint64_t gstart, gend;
+  };
+
+ private:
+  void sync(const void* kernel, cudaStream_t s);
+  std::vector<Entry> host_;
+  std::vector<uint32_t> first_;  // first entry of every CTA for grid_
+  std::vector<uint8_t> vec_;
+  uint64_t groups_ = 0;
+  int grid_ = 0;
+  void* dev_ = nullptr;
+  int dev_device_ = -1;
+  std::vector<unsigned char> shadow_;  // what dev_ holds
+  uint64_t uploads_ = 0;
+};
+
+// Launch accounting and optional per-launch CUDA-event timing (roofline).
+enum KernelKind { kKernPack = 0, kKernSum = 1, kKernSgd = 2, kKernSynth = 3, kKernChecksum = 4, kKernKinds = 5 };
+struct KernelStats {
+  uint64_t launches = 0;
+  double total_ms = 0.0;  // summed CUDA-event durations (profiling on only)
+  double bytes = 0.0;     // algorithmic bytes moved by those launches
+};
+uint64_t launch_count();
+void profile_enable(bool on);
+KernelStats profile_collect(int kind);  // synchronizes pending timing events
+void profile_reset();
 
 }  // namespace csb

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "hostprof.hpp"
 #include "kernels.hpp"
 
 namespace csb {
@@ -68,9 +69,14 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   init_order_tag_ = engine_.new_variable();
   if (cfg_.mode == KvMode::DepCha) dummy_tag_ = engine_.new_variable();
   if (cfg_.mode == KvMode::Funnel) funnel_tag_ = engine_.new_variable();
+  // Lanes: packs, collectives (one ordered stream per communicator) and
+  // unpack/update run on separate CUDA streams, so bucket b's update
+  // overlaps bucket b+1's collective; the engine's events order each key.
   world_lane_ = engine_.new_lane(cfg_.comm_priority);
   if (cfg_.mode == KvMode::ConCom)
     for (int i = 0; i < cfg_.outstanding; ++i) comm_lanes_.push_back(engine_.new_lane(cfg_.comm_priority));
+  pack_lane_ = engine_.new_lane(cfg_.comm_priority);
+  update_lane_ = engine_.new_lane(0);
 }
 
 KvStore::~KvStore() {
@@ -108,6 +114,14 @@ int KvStore::bucket_lane(int b) const {
   return buckets_[static_cast<size_t>(b)].lane;
 }
 
+std::vector<std::vector<int>> KvStore::bucket_groups() {
+  build_buckets();
+  std::vector<std::vector<int>> g;
+  for (const Bucket& b : buckets_) g.push_back(b.keys);
+  if (cfg_.bucket_bytes == 0 && cfg_.issue_order) std::reverse(g.begin(), g.end());
+  return g;
+}
+
 void* KvStore::key_ptr(int key) const {
   const KeyState& k = keys_[static_cast<size_t>(key)];
   const Bucket& b = buckets_[static_cast<size_t>(k.bucket)];
@@ -124,7 +138,6 @@ void KvStore::init(int key, TensorSlot weights) {
   dtype_size(weights.dtype);
   ks.numel = weights.numel;
   ks.wdtype = weights.dtype;
-  ks.buf_tag = engine_.new_variable();
   ks.initialized = true;
   ++initialized_count_;
 
@@ -133,6 +146,7 @@ void KvStore::init(int key, TensorSlot weights) {
     engine_.bind_device();
     Bucket b;
     b.keys = {key};
+    b.tag = engine_.new_variable();
     b.count = ks.numel;
     b.base = device_alloc_zeroed(ks.numel * dtype_size(comm_dt_));
     allocations_.push_back(b.base);
@@ -203,6 +217,7 @@ void KvStore::build_buckets() {
   uint64_t off = 0;
   for (size_t i = 0; i < bs.size(); ++i) {
     Bucket& b = bs[i];
+    b.tag = engine_.new_variable();
     b.base = arena + off * es;
     off += b.count;
     if (cfg_.mode == KvMode::ConCom) {
@@ -230,15 +245,17 @@ std::vector<std::pair<int, std::vector<int>>> KvStore::group_by_bucket(
 }
 
 void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& grads) {
+  hostprof::Scope prof(hostprof::kKvPush);
   if (keys.size() != grads.size()) throw UsageError("KvStore: keys and values differ in length");
+  const uint32_t stamp = next_stamp();
   for (size_t i = 0; i < keys.size(); ++i) {
     check_key(keys[i], true);
     const KeyState& ks = keys_[static_cast<size_t>(keys[i])];
     if (grads[i].numel != ks.numel)
       throw UsageError("KvStore: pushed gradient shape differs from init shape");
     if (ks.pushed) throw UsageError("KvStore: key pushed twice without a pull");
-    for (size_t j = 0; j < i; ++j)
-      if (keys[j] == keys[i]) throw UsageError("KvStore: duplicate key in one push");
+    if (seen_[static_cast<size_t>(keys[i])] == stamp) throw UsageError("KvStore: duplicate key in one push");
+    seen_[static_cast<size_t>(keys[i])] = stamp;
   }
   build_buckets();
 
@@ -256,16 +273,18 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
       if (g.dtype != src_dt) throw UsageError("KvStore: one push mixes gradient dtypes in a bucket");
       entries.push_back(cs_copy_entry{g.data, key_ptr(k), g.numel});
       reads.push_back(g.tag);
-      muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
       keys_[static_cast<size_t>(k)].pushed = true;
     }
+    muts.push_back(B.tag);
     const int dst_dt = comm_dt_;
     const int key0 = keys[static_cast<size_t>(idxs[0])];
+    if (!B.pack_tab) B.pack_tab = std::make_shared<DeviceTable>();
+    DeviceTable* tab = B.pack_tab.get();  // resident table; all its launches on pack_lane_
     engine_.push_stream(
-        [entries, src_dt, dst_dt](cudaStream_t s) {
-          pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
+        [entries, src_dt, dst_dt, tab](cudaStream_t s) {
+          tab->pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
         },
-        reads, muts, OpKind::Copy, key0, B.lane, Dispatch::Inline);
+        reads, muts, OpKind::Copy, key0, pack_lane_, Dispatch::Inline);
     B.pushed += static_cast<int>(idxs.size());
 
     if (B.pushed == static_cast<int>(B.keys.size()) &&
@@ -276,8 +295,7 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
 
 void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
   Bucket& B = buckets_[static_cast<size_t>(b)];
-  std::vector<Tag> muts;
-  for (int k : B.keys) muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
+  std::vector<Tag> muts{B.tag};
   Transport* tr = &transport_;
   const int rank = rank_;
   const int key0 = B.keys[0];
@@ -337,14 +355,16 @@ void KvStore::ensure_momentum(int key, int wdt) {
 
 void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSlot>& outs,
                         const SgdConfig* sgd) {
+  hostprof::Scope prof(hostprof::kKvPull);
   if (keys.size() != outs.size()) throw UsageError("KvStore: keys and values differ in length");
+  const uint32_t stamp = next_stamp();
   for (size_t i = 0; i < keys.size(); ++i) {
     check_key(keys[i], true);
     const KeyState& ks = keys_[static_cast<size_t>(keys[i])];
     if (!ks.pushed) throw UsageError("KvStore: pull without a preceding push this iteration");
     if (outs[i].numel != ks.numel) throw UsageError("KvStore: pull output shape differs from init shape");
-    for (size_t j = 0; j < i; ++j)
-      if (keys[j] == keys[i]) throw UsageError("KvStore: duplicate key in one pull");
+    if (seen_[static_cast<size_t>(keys[i])] == stamp) throw UsageError("KvStore: duplicate key in one pull");
+    seen_[static_cast<size_t>(keys[i])] = stamp;
   }
   const bool momentum = sgd && sgd->momentum != 0.0;
 
@@ -352,7 +372,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     Bucket& B = buckets_[static_cast<size_t>(b)];
     if (B.pushed != static_cast<int>(B.keys.size()))
       throw UsageError("KvStore: pull of a fusion bucket before all of its keys were pushed");
-    std::vector<Tag> buf_tags, out_tags;
+    std::vector<Tag> buf_tags{B.tag}, out_tags;
     std::vector<cs_copy_entry> copies;
     std::vector<cs_update_entry> updates;
     int out_dt = -1;
@@ -361,7 +381,6 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       const TensorSlot& o = outs[static_cast<size_t>(i)];
       if (out_dt < 0) out_dt = o.dtype;
       if (o.dtype != out_dt) throw UsageError("KvStore: one pull mixes output dtypes in a bucket");
-      buf_tags.push_back(keys_[static_cast<size_t>(k)].buf_tag);
       out_tags.push_back(o.tag);
       if (sgd) {
         if (momentum) ensure_momentum(k, o.dtype);
@@ -373,21 +392,27 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     const int cdt = comm_dt_;
     const SgdConfig opt = sgd ? *sgd : SgdConfig{};
     const bool upd = sgd != nullptr;
-    // unpack (kvstore.cpp:160/170 copy) or the fused SGD update, kernel (a)/(c)
-    auto finish = [copies, updates, cdt, out_dt, opt, upd](cudaStream_t s) {
-      if (upd) sgd_update(updates.data(), static_cast<int>(updates.size()), out_dt, cdt, opt.lr,
-                          opt.rescale, opt.momentum, s);
-      else pack(copies.data(), static_cast<int>(copies.size()), cdt, out_dt, s);
+    // unpack (kvstore.cpp:160/170 copy) or the fused SGD update, kernel (a)/(c),
+    // through the bucket's resident tables (all launched on update_lane_)
+    if (!B.upd_tab) B.upd_tab = std::make_shared<DeviceTable>();
+    if (!B.unpack_tab) B.unpack_tab = std::make_shared<DeviceTable>();
+    DeviceTable* utab = B.upd_tab.get();
+    DeviceTable* ctab = B.unpack_tab.get();
+    auto finish = [copies, updates, cdt, out_dt, opt, upd, utab, ctab](cudaStream_t s) {
+      if (upd) utab->sgd(updates.data(), static_cast<int>(updates.size()), out_dt, cdt, opt.lr,
+                         opt.rescale, opt.momentum, s);
+      else ctab->pack(copies.data(), static_cast<int>(copies.size()), cdt, out_dt, s);
     };
     const int key0 = keys[static_cast<size_t>(idxs[0])];
 
     if ((cfg_.mode == KvMode::DepCha || cfg_.mode == KvMode::Naive) && !B.issued) {
-      // one op {allreduce; copy-out} (kvstore.cpp:163-179).  The allreduce
-      // rewrites the comm buffer, so it is modelled as a write (the
-      // reference holds only a read grant there).
-      std::vector<Tag> muts;
-      for (int k : B.keys) muts.push_back(keys_[static_cast<size_t>(k)].buf_tag);
-      for (const Tag& t : out_tags) muts.push_back(t);
+      // the reference pushes one op {allreduce; copy-out} mutating {out,
+      // dummy} (kvstore.cpp:163-179).  Here the collective is its own op on
+      // the ordered comm stream -- it rewrites the comm buffer, so it is
+      // modelled as a write (the reference holds only a read grant there) --
+      // and carries the dummy tag, so collectives stay chained in push order;
+      // the copy-out / update follows as an op on the update lane.
+      std::vector<Tag> muts{B.tag};
       if (cfg_.mode == KvMode::DepCha) muts.push_back(dummy_tag_);
       Transport* tr = &transport_;
       const int rank = rank_;
@@ -397,15 +422,13 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       const int bid = cfg_.bucket_bytes ? b : -1;
       B.issued = true;
       engine_.push_stream(
-          [tr, rank, base, count, cdt, ckey, bid, finish](cudaStream_t s) {
+          [tr, rank, base, count, cdt, ckey, bid](cudaStream_t s) {
             tr->allreduce_sum(Transport::world(), rank, base, count, cdt, ckey, s, bid);
-            finish(s);
           },
           {}, muts, OpKind::Collective, ckey, B.lane, Dispatch::Pool);
-    } else {
-      engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
-                          B.lane, Dispatch::Inline);
     }
+    engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
+                        update_lane_, Dispatch::Inline);
     for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;
     B.pulled += static_cast<int>(idxs.size());
     if (B.pulled == static_cast<int>(B.keys.size())) {
@@ -428,7 +451,7 @@ void KvStore::comm_buf(int key, void* host_out) {
   check_key(key, true);
   const KeyState& ks = keys_[static_cast<size_t>(key)];
   if (ks.bucket < 0) throw UsageError("KvStore: comm buffer not allocated yet");
-  engine_.wait_for(ks.buf_tag);
+  engine_.wait_for(buckets_[static_cast<size_t>(ks.bucket)].tag);
   engine_.bind_device();
   CSB_CUDA(cudaMemcpy(host_out, key_ptr(key), ks.numel * dtype_size(comm_dt_), cudaMemcpyDeviceToHost));
 }

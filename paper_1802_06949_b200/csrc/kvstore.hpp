@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "kernels.hpp"
 #include "transport.hpp"
 
 namespace csb {
@@ -87,6 +88,8 @@ class KvStore {
   void key_map(int key, int* bucket, uint64_t* offset) const;
   int num_buckets() const { return static_cast<int>(buckets_.size()); }
   int bucket_lane(int b) const;
+  // Keys of every comm bucket, buckets in issue order (builds the map).
+  std::vector<std::vector<int>> bucket_groups();
 
  private:
   struct KeyState {
@@ -96,7 +99,6 @@ class KvStore {
     bool pushed = false;
     int bucket = -1;
     uint64_t offset = 0;  // elements into the bucket buffer
-    Tag buf_tag;
     void* mom = nullptr;  // momentum state (lazy)
   };
   struct Bucket {
@@ -108,6 +110,8 @@ class KvStore {
     bool issued = false;  // collective issued this iteration
     int comm = 0;
     int lane = 0;
+    Tag tag;  // engine tag of the whole comm buffer
+    std::shared_ptr<DeviceTable> pack_tab, upd_tab, unpack_tab;  // resident kernel tables
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -129,12 +133,20 @@ class KvStore {
   std::vector<Bucket> buckets_;
   std::vector<void*> allocations_;
   int world_lane_ = 0;
+  int pack_lane_ = 0;
+  int update_lane_ = 0;
   std::vector<int> comm_lanes_;  // concom: lane per extra communicator
   Tag init_order_tag_;
   Tag dummy_tag_;
   Tag funnel_tag_;
   int initialized_count_ = 0;
   bool built_ = false;
+  std::vector<uint32_t> seen_;  // duplicate-key detection in one call
+  uint32_t stamp_ = 0;
+  uint32_t next_stamp() {
+    if (seen_.size() != keys_.size()) seen_.assign(keys_.size(), 0);
+    return ++stamp_;
+  }
   std::atomic<int> outstanding_{0};
 };
 

@@ -1,6 +1,7 @@
 // transport.cpp -- see transport.hpp.
 #include "transport.hpp"
 
+#include "hostprof.hpp"
 #include "kernels.hpp"
 
 namespace csb {
@@ -206,7 +207,11 @@ void Transport::run(int comm, int rank, const CallSig& sig, void* buf, int trace
       CSB_CUDA(cudaEventRecord(sd->ready[rank], stream));
     };
   }
-  Ledger::Ticket t = ledger_->arrive(comm, rank, sig, trace_key, bucket, publish);
+  Ledger::Ticket t;
+  {
+    hostprof::Scope prof(hostprof::kLedger);
+    t = ledger_->arrive(comm, rank, sig, trace_key, bucket, publish);
+  }
   if (t.last) {
     try {
       if (backend_ == Backend::Local && sig.kind != CollKind::Barrier) local_data(t, sig, buf, stream);
@@ -224,7 +229,9 @@ void Transport::run(int comm, int rank, const CallSig& sig, void* buf, int trace
     }
     CSB_CUDA(cudaStreamWaitEvent(stream, sd->done, 0));
   }
-  if (backend_ == Backend::Nccl && sig.kind != CollKind::Barrier && sig.count > 0) {
+  // one rank: the matched call is the identity (collective.cpp:228-243 with
+  // R = 1), nothing to move
+  if (backend_ == Backend::Nccl && sig.kind != CollKind::Barrier && sig.count > 0 && num_ranks() > 1) {
     device_latency(stream);
     nccl_data(comm, sig, buf, stream);
   }

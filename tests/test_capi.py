@@ -1,0 +1,83 @@
+"""The drop-in boundary: libcollsim_b200.so loads (no GPU needed) and exports
+every entry point include/collsim_b200.h declares; status codes map to the
+reference error kinds (R/core/include/collsim/error.hpp:10-31).  CPU only."""
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "collsim_b200.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:int|char\s*\*|const char\s*\*)\s+\**\s*(cs_\w+)\s*\(",
+                                 text, flags=re.M)))
+
+
+def test_header_declares_entry_points():
+    names = declared_functions()
+    assert len(names) > 50
+    for must in ("cs_pack", "cs_sum_buffers", "cs_sgd_update", "cs_engine_push_stream", "cs_allreduce_sum",
+                 "cs_kv_push", "cs_kv_pull", "cs_kv_pull_update", "cs_create_communicators"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1802_06949_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+    # and the ctypes table binds exactly the declared set
+    assert sorted(_lib.SIGNATURES) == declared_functions()
+
+
+def test_library_is_sm100a_only():
+    from paper_1802_06949_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_\d+a?", out))
+    assert arches == {"sm_100a"}, arches
+
+
+def test_status_names_mirror_reference_error_kinds():
+    from paper_1802_06949_b200._lib import lib
+    names = {s: lib.cs_status_name(s).decode() for s in range(-8, 1)}
+    assert names[0] == "OK"
+    assert names[-1] == "ConfigError" and names[-2] == "UsageError" and names[-3] == "MismatchError"
+    assert names[-4] == "DeadlockTimeout" and names[-5] == "EngineError"
+
+
+def test_errors_cross_the_boundary_as_status_codes():
+    from paper_1802_06949_b200 import ConfigError, Engine, Transport, UsageError
+    with pytest.raises(ConfigError):
+        Engine(0)  # engine.cpp:23-25
+    with pytest.raises(ConfigError):
+        Transport.ledger_only(0)
+    with pytest.raises(ConfigError):
+        Transport.ledger_only(2, watchdog_ms=0)
+    e = Engine(1)
+    with pytest.raises(UsageError):
+        e.push_stream(lambda s: None)  # host-only engine: no lanes
+    with pytest.raises(UsageError):
+        e.wait_for(12345)  # unknown tag
+
+
+def test_kernels_reject_bad_arguments_without_a_gpu():
+    from paper_1802_06949_b200 import UsageError, api
+    with pytest.raises(UsageError):
+        api.sum_buffers([], [1], 10, api.F32)
+    with pytest.raises(UsageError):
+        api.sum_buffers([1] * 17, [1], 10, api.F32)
+    with pytest.raises(UsageError):
+        api.sgd_update([(16, 32, 0, 4)], api.F32, api.F32, 0.1, 1.0, 0.9)  # momentum needs a buffer
+
+
+def test_device_count_is_zero_here_or_positive_on_box():
+    from paper_1802_06949_b200 import device_count
+    assert device_count() >= 0

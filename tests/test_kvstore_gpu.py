@@ -383,6 +383,8 @@ def test_naive_hazard_and_depcha_safety(gpu):
     """acceptance.cpp:211-238: naive (4 engine threads) trips the ledger in
     >= 1 of N runs; depcha on the same shape never errors.  The hazard is
     caught by the matching ledger BEFORE any device collective is enqueued."""
+    import random
+    import time as _time
     hazards, depcha_errors = 0, 0
     for seed in range(1, 11):
         for mode in ("naive", "depcha"):
@@ -390,12 +392,21 @@ def test_naive_hazard_and_depcha_safety(gpu):
             K = 8
 
             def body(rank, eng, store):
-                ws = [slot(eng, t64(np.zeros(3))) for _ in range(K)]
-                gs = [slot(eng, t64(np.full(3, float(rank)))) for _ in range(K)]
+                # distinct key sizes (as the diamond model's): a crossed key
+                # pairing is a signature (count) mismatch the ledger catches
+                ws = [slot(eng, t64(np.zeros(3 + k))) for k in range(K)]
+                gs = [slot(eng, t64(np.full(3 + k, float(rank)))) for k in range(K)]
                 for k in range(K):
                     store.init(k, ws[k])
                 eng.wait_all()
+                rng = random.Random(seed * 10 + rank)
                 for _ in range(2):
+                    # backward stage ops (host bodies) finish in a per-rank
+                    # random order, as the reference's compute ops do; naive
+                    # collectives then become ready in different orders
+                    for k in reversed(range(K)):
+                        d = rng.random() * 0.004
+                        eng.push(lambda d=d: _time.sleep(d), [], [gs[k].tag], api.COMPUTE, k)
                     for k in range(K):
                         store.push(k, gs[k])
                     for k in range(K):
