@@ -43,14 +43,28 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "aggregated gradient GB/s/GPU & exposed comm ms/iter at 1/2/4/8 B200"
 CONFIGS = {
-    # name: (keyset, mode, outstanding, dtype, bucket_mb, backward_ms)
-    "resnet50": ("resnet50", "depcha", 1, "fp32", 25, 24.0),
-    "alexnet": ("alexnet", "concom", 4, "fp32", 25, 20.0),
-    "resnet152": ("resnet152", "depcha", 1, "bf16", 25, 60.0),
+    # name: (keyset, mode, outstanding, dtype, bucket_mb, backward calibration or fixed ms)
+    "resnet50": ("resnet50", "depcha", 1, "fp32", 25, "resnet50_b64.json"),
+    "alexnet": ("alexnet", "concom", 4, "fp32", 25, "alexnet_b64_amp.json"),
+    "resnet152": ("resnet152", "depcha", 1, "bf16", 25, "resnet152_b64_amp.json"),
     "inception_v3": ("inception_v3", "depcha", 1, "bf16", 25, 30.0),
     "stress": ("stress", "depcha", 1, "fp32", 64, 0.0),
     "uniform16": ("uniform16x1048576", "funnel", 1, "fp32", 0, 0.0),
 }
+CALIB = ROOT / "paper_1802_06949_b200" / "calibration"
+
+
+def backward_profile(spec, keys):
+    """-> (ready_ms per key or None, backward ms, description).  Calibration
+    files hold per-parameter gradient-ready times measured on a B200 with a
+    real torchvision backward (tools/calibrate_backward.py, batch 64)."""
+    if isinstance(spec, str):
+        d = json.loads((CALIB / spec).read_text())
+        if d["sizes"] != keys:
+            raise SystemExit(f"calibration {spec} does not match the key set")
+        return d["ready_ms"], d["backward_ms"], f"measured {d['model']} batch {d['batch']} " \
+            f"{'bf16 AMP' if d['amp'] else 'fp32/TF32'} backward on {d['gpu']} ({spec})"
+    return None, float(spec), f"fixed {spec} ms split in proportion to key size"
 
 
 def parse():
@@ -192,13 +206,14 @@ def reference_main(args, cfg_name, keys, mode, outstanding, config):
 
 def main():
     args = parse()
-    keyset, mode, outstanding, dtype, bucket_mb, bwd_ms = CONFIGS[args.config]
+    keyset, mode, outstanding, dtype, bucket_mb, bwd_spec = CONFIGS[args.config]
     mode = args.mode or mode
     outstanding = args.outstanding or outstanding
     bucket_mb = args.bucket_mb if args.bucket_mb is not None else bucket_mb
-    bwd_ms = args.backward_ms if args.backward_ms is not None else bwd_ms
     from paper_1802_06949_b200 import keysets
     keys = keysets.load(keyset)
+    ready_ms, bwd_ms, bwd_desc = backward_profile(
+        args.backward_ms if args.backward_ms is not None else bwd_spec, keys)
     rank, local_rank, world = dist_env()
     config = {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
               "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
@@ -239,7 +254,8 @@ def main():
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5)
-    model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, **common)
+    model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, ready_ms=ready_ms,
+                           **common)
     model.init()
     info = model.info()
     gbytes = info["grad_bytes"]
@@ -294,7 +310,8 @@ def main():
         line["step_with_backward_ms"] = round(t_full, 4)
         line["backward_plus_update_ms"] = round(t_comp, 4)
         line["exposed_frac"] = round((t_full - t_comp) / t_full, 4) if t_full > 0 else None
-        line["synthetic_backward_ms"] = bwd_ms
+        line["synthetic_backward_ms"] = round(bwd_ms, 3)
+        line["synthetic_backward"] = bwd_desc
 
         # ---- roofline of the dominant kernel (CUDA events on the launch stream)
         api.profile_reset()

@@ -223,6 +223,11 @@ enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,
                     const uint64_t* sizes, int num_keys, const int* concom_comms, int n_comms,
                     cs_synth_t* out);
+/* same, with the measured gradient-ready time of every key (ms from the start
+ * of a real backward, tools/calibrate_backward.py) driving the producers */
+int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nranks,
+                             const cs_synth_config* cfg, const uint64_t* sizes, const double* ready_ms,
+                             int num_keys, const int* concom_comms, int n_comms, cs_synth_t* out);
 int cs_synth_destroy(cs_synth_t s);
 int cs_synth_init(cs_synth_t s);
 int cs_synth_step(cs_synth_t s, int flags);

@@ -108,6 +108,8 @@ SIGNATURES = {
     "cs_kv_num_buckets": [_P, _PI],
     "cs_kv_bucket_lane": [_P, _I, _PI],
     "cs_synth_create": [_P, _P, _I, _I, C.c_void_p, _PU64, _I, _PI, _I, C.POINTER(_P)],
+    "cs_synth_create_profiled": [_P, _P, _I, _I, C.c_void_p, _PU64, C.POINTER(C.c_double), _I, _PI, _I,
+                                 C.POINTER(_P)],
     "cs_synth_destroy": [_P],
     "cs_synth_init": [_P],
     "cs_synth_step": [_P, _I],

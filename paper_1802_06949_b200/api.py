@@ -488,15 +488,17 @@ class SynthModel:
                  bucket_bytes: int = 0, issue_order: int = 0, outstanding: int = 1, lr: float = 0.1,
                  rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
                  backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0,
-                 host_source: bool = False, concom_comms: Sequence[int] = ()):
+                 host_source: bool = False, concom_comms: Sequence[int] = (),
+                 ready_ms: Sequence[float] | None = None):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
                                 int(fused_update), comm_priority, int(host_source))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()
-        check(lib.cs_synth_create(engine.h, transport.h, rank, nranks, C.byref(cfg), sz, len(sizes),
-                                  comms, len(concom_comms), C.byref(h)))
+        rd = (C.c_double * len(sizes))(*ready_ms) if ready_ms is not None else None
+        check(lib.cs_synth_create_profiled(engine.h, transport.h, rank, nranks, C.byref(cfg), sz, rd,
+                                           len(sizes), comms, len(concom_comms), C.byref(h)))
         self.h = h
         self.engine = engine
         self.transport = transport

@@ -488,6 +488,39 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     *out = h.release();
   });
 }
+int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nranks,
+                             const cs_synth_config* cfg, const uint64_t* sizes, const double* ready_ms,
+                             int num_keys, const int* concom_comms, int n_comms, cs_synth_t* out) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    CHECK_HANDLE(t);
+    CHECK_HANDLE(cfg);
+    if (num_keys < 1 || !sizes) throw ConfigError("synth: no keys");
+    if (cfg->mode < 0 || cfg->mode > 3) throw ConfigError("unknown kvstore mode");
+    SynthConfig c;
+    c.mode = static_cast<KvMode>(cfg->mode);
+    c.sizes.assign(sizes, sizes + num_keys);
+    if (ready_ms) c.ready_ms.assign(ready_ms, ready_ms + num_keys);
+    c.wdt = cfg->w_dtype;
+    c.gdt = cfg->g_dtype;
+    c.cdt = cfg->comm_dtype;
+    c.bucket_bytes = cfg->bucket_bytes;
+    c.issue_order = cfg->issue_order;
+    c.outstanding = cfg->outstanding;
+    c.lr = cfg->lr;
+    c.rescale = cfg->rescale;
+    c.momentum = cfg->momentum;
+    c.backward_ns = cfg->backward_ns;
+    c.backward_ctas = cfg->backward_ctas;
+    c.fused = cfg->fused_update != 0;
+    c.comm_priority = cfg->comm_priority;
+    c.host_source = cfg->host_source != 0;
+    std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
+    auto h = std::make_unique<cs_synth>();
+    h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
+    *out = h.release();
+  });
+}
 int cs_synth_destroy(cs_synth_t s) {
   return guard([&] { delete s; });
 }

@@ -75,6 +75,7 @@ struct LedgerShared {
   pthread_mutex_t mu;
   pthread_cond_t cv;
   int32_t comms_by_rank[kLedgerMaxRanks];
+  int32_t started_by_rank[kLedgerMaxRanks];
   uint64_t next_seq[kLedgerMaxComms][kLedgerMaxRanks];
   InflightRec inflight[kLedgerMaxRanks * kInflightPerRank];
   int32_t blob_ready[kLedgerMaxComms];
@@ -248,7 +249,9 @@ Ledger::~Ledger() {
 
 int Ledger::new_communicator() {
   Lock lk(s_);
-  if (s_->started)
+  // setup-phase only (collective.cpp:44-51); with one process per rank the
+  // phase is per process: this rank must not have issued a collective yet
+  if (shm_ ? s_->started_by_rank[rank_] : s_->started)
     throw UsageError(
         "Transport: communicators must be created before workers start issuing collectives");
   if (shm_) {
@@ -359,6 +362,7 @@ Ledger::Ticket Ledger::arrive(int comm, int rank, const CallSig& sig, int trace_
   if (comm < 0 || comm >= s_->ncomms) throw UsageError("collective: unknown communicator");
   if (s_->latched) throw_latched();
   s_->started = 1;
+  s_->started_by_rank[rank] = 1;
 
   const uint64_t seq = s_->next_seq[comm][rank]++;
   const int slot = static_cast<int>(seq % kLedgerSlots);

@@ -147,11 +147,23 @@ void SynthModel::init() {
   uint64_t total = 0;
   for (uint64_t n : cfg_.sizes) total += n;
   spin_ns_.resize(K);
-  for (int k = 0; k < K; ++k)
-    spin_ns_[k] = cfg_.backward_ns == 0
-                      ? 0
-                      : std::max<uint64_t>(2000, static_cast<uint64_t>(static_cast<double>(cfg_.backward_ns) *
-                                                                       cfg_.sizes[k] / total));
+  produce_order_.resize(K);
+  for (int k = 0; k < K; ++k) produce_order_[k] = K - 1 - k;  // backward: last layer first
+  if (static_cast<int>(cfg_.ready_ms.size()) == K) {
+    std::stable_sort(produce_order_.begin(), produce_order_.end(),
+                     [&](int a, int b) { return cfg_.ready_ms[a] < cfg_.ready_ms[b]; });
+    double prev = 0.0;
+    for (int k : produce_order_) {
+      spin_ns_[k] = static_cast<uint64_t>(std::max(0.0, cfg_.ready_ms[k] - prev) * 1e6);
+      prev = std::max(prev, cfg_.ready_ms[k]);
+    }
+  } else {
+    for (int k = 0; k < K; ++k)
+      spin_ns_[k] = cfg_.backward_ns == 0
+                        ? 0
+                        : std::max<uint64_t>(2000, static_cast<uint64_t>(static_cast<double>(cfg_.backward_ns) *
+                                                                         cfg_.sizes[k] / total));
+  }
   for (int k = 0; k < K; ++k) {
     w_.push_back(w_arena_ + woff[k]);
     g_.push_back(g_arena_ + goff[k]);
@@ -181,7 +193,7 @@ void SynthModel::enqueue_step(int flags) {
         },
         {}, gt_, OpKind::Copy, -1, 0, Dispatch::Inline);
   } else if (flags & kStepBackward) {
-    for (int k = K - 1; k >= 0; --k) {
+    for (int k : produce_order_) {
       void* dst = g_[k];
       const void* src = src_[k];
       const uint64_t n = cfg_.sizes[k];

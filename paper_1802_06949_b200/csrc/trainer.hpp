@@ -36,6 +36,11 @@ struct SynthConfig {
   int comm_priority = 0;
   bool host_source = false;  // gradients arrive from pinned host memory (e2e)
   uint64_t seed_base = 1000;
+  // Measured gradient-ready time of every key from the start of a real
+  // backward (tools/calibrate_backward.py).  When set, producers run in
+  // ready order and key k holds the device for ready[k] - ready[previous],
+  // replacing the size-proportional split of backward_ns.
+  std::vector<double> ready_ms;
 };
 
 enum SynthFlags {
@@ -73,6 +78,7 @@ class SynthModel {
   std::vector<void*> w_, g_, src_;
   std::vector<Tag> wt_, gt_;
   std::vector<uint64_t> spin_ns_;
+  std::vector<int> produce_order_;  // producer order (descending keys or measured ready order)
   char* w_arena_ = nullptr;
   uint64_t w_arena_elems_ = 0;
   char* g_arena_ = nullptr;

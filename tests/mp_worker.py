@@ -1,0 +1,139 @@
+"""One rank of a multi-process (one process per GPU) scenario over the NCCL
+transport; launched by tests/test_nccl_multigpu.py through torchrun.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/mp_worker.py <case> <outdir>
+
+Writes <outdir>/<case>_r<rank>.npz / .json; the test compares them with the
+oracle and the golden fixtures.  torch.distributed (gloo) is plumbing only:
+it passes the ledger name and joins the ranks at the end.
+"""
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+sys.path.insert(0, str(HERE))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import _oracle as O  # noqa: E402
+from paper_1802_06949_b200 import (DeadlockTimeout, Engine, KvConfig, KvStore, MismatchError,  # noqa: E402
+                                   Slot, TraceSink, Transport, api, create_communicators)
+
+
+def t64(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def main():
+    case, outdir = sys.argv[1], Path(sys.argv[2])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    name = [f"csb_test_{os.getpid()}_{time.time_ns() % 10**9}"]
+    dist.broadcast_object_list(name, src=0)
+    sink = TraceSink()
+    watchdog = 3000 if case in ("mismatch", "deadlock") else 60000
+    tr = Transport.nccl(name[0], world, rank, local, watchdog, sink)
+    out = {}
+
+    if case == "allreduce":
+        # acceptance criterion 1 inputs (acceptance.cpp:42-84), fp64
+        eng = Engine(2, rank, None, local)
+        s = eng.lane_stream(0)
+        res = []
+        for i in range(100):
+            n = 1 + (i * 7) % 64
+            b = t64(O.random_uniform(n, O.mix_seed(world * 1000 + i, rank)), dev)
+            tr.allreduce_sum(0, rank, b, i, s)
+            res.append(b)
+        torch.cuda.synchronize(dev)
+        eng.wait_all()
+        np.savez(outdir / f"{case}_r{rank}.npz", *[x.cpu().numpy() for x in res])
+        eng.close()
+    elif case in ("funnel", "depcha", "concom"):
+        gold = np.load(HERE / "golden" / "train_steps.npz")
+        sizes = [int(x) for x in gold["sizes"]]
+        K, lr, rescale = len(sizes), float(gold["lr"]), 1.0 / (64 * world)
+        outstanding = 2 if case == "concom" else 1
+        comms = create_communicators(tr, outstanding) if case == "concom" else []
+        eng = Engine(4, rank, sink, local)
+        store = KvStore(eng, tr, rank, KvConfig(case, outstanding, K), comms)
+        ws = [Slot(t64(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n), dev),
+                   eng.new_variable()) for k, n in enumerate(sizes)]
+        gs = [Slot(t64(O.random_uniform(n, 1000 + rank * K + k), dev), eng.new_variable())
+              for k, n in enumerate(sizes)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        src = [g.value.clone() for g in gs]
+        for _ in range(3):
+            for k in reversed(range(K)):
+                sp, dp, n = src[k].data_ptr(), gs[k].value.data_ptr(), sizes[k]
+                eng.push_stream(lambda st, sp=sp, dp=dp, n=n: api.synth_backward(sp, dp, n, api.F64, 0, 0, st),
+                                [], [gs[k].tag], api.COMPUTE, k)
+            if case == "depcha":
+                store.push(list(range(K)), gs)
+                store.pull_update(list(range(K)), ws, lr, rescale)
+            else:
+                since = 0
+                for k in range(K):
+                    store.push(k, gs[k])
+                    store.pull_update(k, ws[k], lr, rescale)
+                    if case == "concom":
+                        since += 1
+                        if since == outstanding:
+                            store.barrier()
+                            since = 0
+                if case == "concom" and since:
+                    store.barrier()
+            eng.wait_all()
+        np.savez(outdir / f"{case}_r{rank}.npz", *[w.value.cpu().numpy() for w in ws])
+        store.close()
+        eng.close()
+    elif case == "mismatch":
+        eng = Engine(1, rank, None, local)
+        b = torch.zeros(4 if rank == 0 else 6, dtype=torch.float64, device=dev)
+        try:
+            tr.allreduce_sum(0, rank, b, 0, eng.lane_stream(0))
+            out["error"] = None
+        except MismatchError as e:
+            out["error"] = "MismatchError"
+            out["message"] = str(e)
+        eng.close()
+    elif case == "deadlock":
+        eng = Engine(1, rank, None, local)
+        b = torch.zeros(4, dtype=torch.float64, device=dev)
+        try:
+            if rank == 0:
+                tr.allreduce_sum(0, rank, b, 0, eng.lane_stream(0))
+            else:
+                time.sleep(5)  # never issues its call
+            out["error"] = None
+        except DeadlockTimeout as e:
+            out["error"] = "DeadlockTimeout"
+            out["message"] = str(e)
+        eng.close()
+    else:
+        raise SystemExit(f"unknown case {case}")
+
+    if case in ("funnel", "depcha", "concom"):
+        out["trace"] = [f"{e['kind']}:{e['comm']}:{e['seq']}:{e.get('key', -1)}"
+                        for e in sink.snapshot() if e["event"] == "coll_enqueued"]
+    (outdir / f"{case}_r{rank}.json").write_text(json.dumps(out))
+    dist.barrier()
+    tr.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,94 @@
+"""One process per GPU over NCCL (NVLink): parity of the allreduce and of the
+three schedules against the oracle / golden fixtures, and the cross-process
+matching ledger turning a misordered or missing call into MismatchError /
+DeadlockTimeout before anything is enqueued on NVLink.
+Needs >= 2 GPUs (gpurun --gpus 2); skipped otherwise."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import _oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+HERE = Path(__file__).resolve().parent
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_case(case, n, tmp_path):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(HERE / "mp_worker.py"), case,
+           str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [json.loads((tmp_path / f"{case}_r{i}.json").read_text()) for i in range(n)]
+
+
+def world_sizes(ngpus):
+    return [w for w in (2, 4) if w <= ngpus]
+
+
+def test_nccl_allreduce_acceptance_1(two_gpus, tmp_path):
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("allreduce", R, d)
+        outs = [np.load(d / f"allreduce_r{r}.npz") for r in range(R)]
+        for i in range(100):
+            n = 1 + (i * 7) % 64
+            exp = O.rank_order_sum([O.random_uniform(n, O.mix_seed(R * 1000 + i, r)) for r in range(R)])
+            for r in range(R):
+                got = outs[r][f"arr_{i}"]
+                if R == 2:
+                    np.testing.assert_array_equal(got, exp)  # a + b: order-free, exact
+                else:
+                    assert np.max(np.abs(got - exp)) <= 1e-12  # reference tolerance
+            for r in range(1, R):  # every rank holds the same result
+                np.testing.assert_array_equal(outs[r][f"arr_{i}"], outs[0][f"arr_{i}"])
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+def test_nccl_schedules_match_reference(two_gpus, tmp_path, mode):
+    gold = np.load(HERE / "golden" / "train_steps.npz")
+    K = len(gold["sizes"])
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        outs = run_case(mode, R, d)
+        for r in range(R):
+            w = np.load(d / f"{mode}_r{r}.npz")
+            for k in range(K):
+                exp = gold[f"{mode}_R{R}_r{r}_k{k}"]
+                if R == 2:
+                    np.testing.assert_array_equal(w[f"arr_{k}"], exp)
+                else:
+                    np.testing.assert_allclose(w[f"arr_{k}"], exp, rtol=0, atol=1e-12)
+        # identical per-comm issue sequences on every rank
+        for r in range(1, R):
+            for comm in {s.split(":")[1] for s in outs[0]["trace"]}:
+                assert [s for s in outs[r]["trace"] if s.split(":")[1] == comm] == \
+                    [s for s in outs[0]["trace"] if s.split(":")[1] == comm]
+
+
+def test_cross_process_mismatch_raises_before_nccl(two_gpus, tmp_path):
+    outs = run_case("mismatch", 2, tmp_path)
+    assert [o["error"] for o in outs] == ["MismatchError", "MismatchError"]
+    assert "allreduce(count=4)" in outs[0]["message"] and "allreduce(count=6)" in outs[0]["message"]
+
+
+def test_cross_process_deadlock_report(two_gpus, tmp_path):
+    outs = run_case("deadlock", 2, tmp_path)
+    assert outs[0]["error"] == "DeadlockTimeout"
+    assert "rank 1: no call issued" in outs[0]["message"]
