@@ -83,6 +83,8 @@ def parse():
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+                   help="collective engine for N>1: NCCL, or the fused NVLink peer-memory kernel")
     return p.parse_args()
 
 
@@ -92,7 +94,13 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks
+    line).  Each query briefly stalls the driver: at 4 GPUs a query landing
+    inside the ~12 ms timed region was measured to add ~1 ms/step, and an
+    in-process NVML sampler at 10 ms slowed every run.  So the period is
+    200 ms and the timed region starts right after a sample arrives
+    (wait_first); the soak that follows keeps the same steps running so the
+    next samples see this load."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -104,10 +112,12 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("CSB_CLOCKS") == "off":
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -115,9 +125,12 @@ class Clocks:
         return self
 
     def wait_first(self, timeout: float = 5.0):
+        """Returns right after a fresh sample arrived (the next query is
+        ~200 ms away)."""
         t0 = time.time()
-        while self.proc and not self.rows and time.time() - t0 < timeout:
-            time.sleep(0.02)
+        n0 = len(self.rows)
+        while self.proc and len(self.rows) <= max(n0, 0) and time.time() - t0 < timeout:
+            time.sleep(0.001)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -253,7 +266,9 @@ def main():
     common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
-                  backward_ns=int(bwd_ms * 1e6), comm_priority=-5)
+                  backward_ns=int(bwd_ms * 1e6), comm_priority=-5, p2p=args.comm == "p2p")
+    config["collectives"] = "fused NVLink peer-memory allreduce+update" if (args.comm == "p2p" and world > 1) \
+        else ("NCCL" if world > 1 else "identity (1 rank)")
     model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, ready_ms=ready_ms,
                            **common)
     model.init()
@@ -270,6 +285,8 @@ def main():
     l0 = api.launch_count()
     with Clocks(local_rank) as clk:
         clk.wait_first()
+        clk.wait_first()  # aligned to the sampler's period, not its start-up
+        barrier()
         ms = model.run(args.steps, COMM)
         launches = api.launch_count() - l0
         host_ms = model.last_host_ms()

@@ -159,6 +159,23 @@ int cs_allreduce_sum(cs_transport_t t, int comm, int rank, void* buf, uint64_t n
 int cs_broadcast(cs_transport_t t, int comm, int rank, int root, void* buf, uint64_t n,
                  cs_dtype dt, int trace_key, cs_stream_t stream);
 int cs_barrier(cs_transport_t t, int comm, int rank, int trace_key, cs_stream_t stream);
+/* NVLink peer-memory path (NCCL transport, >= 2 peer-capable ranks):
+ * setup-phase collective mapping every rank's allocation `base` (CUDA IPC);
+ * ptrs_out[r] = rank r's buffer as seen from this process. */
+int cs_transport_p2p_capable(cs_transport_t t, int* out);
+int cs_transport_share_buffer(cs_transport_t t, void* base, void** ptrs_out);
+/* allreduce of peer_bufs[*] (n elements, multiple of 8) in rank order, every
+ * rank ends with the sum; with upd != NULL fused with the SGD / momentum
+ * update of the listed weights (entries address the bucket by element
+ * offset: entry.g = &bucket[offset], offset a multiple of 8). */
+typedef struct cs_p2p_update {
+  const cs_update_entry* entries; /* g points into this rank's bucket */
+  int n_entries;
+  int w_dtype;
+  double lr, rescale, momentum;
+} cs_p2p_update;
+int cs_allreduce_p2p(cs_transport_t t, int comm, int rank, void* const* peer_bufs, uint64_t n,
+                     cs_dtype dt, int trace_key, const cs_p2p_update* upd, cs_stream_t stream);
 
 /* ----------------------------------------------------------- kvstore */
 typedef struct cs_kvstore* cs_kvstore_t;
@@ -171,6 +188,9 @@ typedef struct cs_kv_config {
   uint64_t bucket_bytes; /* 0: one comm buffer per key (reference 1:1 map, kvstore.cpp:84) */
   int issue_order;       /* bucket grouping order: 0 ascending keys, 1 descending */
   int comm_priority;     /* CUDA stream priority of the comm lanes (<=0, lower = higher prio) */
+  int p2p;               /* 1: NVLink peer-memory collectives (needs bucket_bytes > 0 and a
+                            peer-capable NCCL transport); DepCha pull_update becomes one fused
+                            allreduce+update kernel per bucket, rank-order (bit-exact) sums */
 } cs_kv_config;
 typedef struct cs_slot { /* TensorSlot (kvstore.hpp:16-19): non-owning device view + tag */
   void* data;
@@ -218,6 +238,7 @@ typedef struct cs_synth_config {
   int fused_update;       /* 1: pull_update (kernel (c) on the reduced bucket) */
   int comm_priority;
   int host_source;        /* 1: gradients copied from pinned host memory each step */
+  int p2p;                /* as cs_kv_config.p2p */
 } cs_synth_config;
 enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,

@@ -31,10 +31,15 @@ class UpdateEntry(C.Structure):
     _fields_ = [("w", C.c_void_p), ("g", C.c_void_p), ("mom", C.c_void_p), ("n", C.c_uint64)]
 
 
+class P2PUpdateC(C.Structure):
+    _fields_ = [("entries", C.c_void_p), ("n_entries", C.c_int), ("w_dtype", C.c_int), ("lr", C.c_double),
+                ("rescale", C.c_double), ("momentum", C.c_double)]
+
+
 class KvConfigC(C.Structure):
     _fields_ = [("mode", C.c_int), ("outstanding", C.c_int), ("num_keys", C.c_int),
                 ("comm_dtype", C.c_int), ("bucket_bytes", C.c_uint64), ("issue_order", C.c_int),
-                ("comm_priority", C.c_int)]
+                ("comm_priority", C.c_int), ("p2p", C.c_int)]
 
 
 class SlotC(C.Structure):
@@ -94,6 +99,9 @@ SIGNATURES = {
     "cs_allreduce_sum": [_P, _I, _I, _P, _U64, _I, _I, _P],
     "cs_broadcast": [_P, _I, _I, _I, _P, _U64, _I, _I, _P],
     "cs_barrier": [_P, _I, _I, _I, _P],
+    "cs_transport_p2p_capable": [_P, _PI],
+    "cs_transport_share_buffer": [_P, _P, C.POINTER(_P)],
+    "cs_allreduce_p2p": [_P, _I, _I, C.POINTER(_P), _U64, _I, _I, C.c_void_p, _P],
     "cs_create_communicators": [_P, _I, _PI],
     "cs_kv_create": [_P, _P, _I, C.POINTER(KvConfigC), _PI, _I, C.POINTER(_P)],
     "cs_kv_destroy": [_P],
@@ -131,7 +139,7 @@ class SynthConfigC(C.Structure):
                 ("bucket_bytes", C.c_uint64), ("issue_order", C.c_int), ("outstanding", C.c_int),
                 ("lr", C.c_double), ("rescale", C.c_double), ("momentum", C.c_double),
                 ("backward_ns", C.c_uint64), ("backward_ctas", C.c_int), ("fused_update", C.c_int),
-                ("comm_priority", C.c_int), ("host_source", C.c_int)]
+                ("comm_priority", C.c_int), ("host_source", C.c_int), ("p2p", C.c_int)]
 
 
 CS_STEP_BACKWARD, CS_STEP_COMM, CS_STEP_LOCAL_UPDATE, CS_STEP_CHECKSUM = 1, 2, 4, 8

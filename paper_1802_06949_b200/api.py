@@ -319,6 +319,29 @@ class Transport:
     def barrier(self, comm: int, rank: int, trace_key: int = -1, stream: int = 0) -> None:
         check(lib.cs_barrier(self.h, comm, rank, trace_key, stream))
 
+    def p2p_capable(self) -> bool:
+        v = C.c_int()
+        check(lib.cs_transport_p2p_capable(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def share_buffer(self, base: int) -> list[int]:
+        n = self.num_ranks()
+        out = (C.c_void_p * n)()
+        check(lib.cs_transport_share_buffer(self.h, base, out))
+        return [p or 0 for p in out]
+
+    def allreduce_p2p(self, comm: int, rank: int, peer_bufs, n: int, dtype: int, trace_key: int = -1,
+                      update=None, stream: int = 0) -> None:
+        """update: (entries[(w, g, mom, n)], w_dtype, lr, rescale, momentum) or None."""
+        bufs = (C.c_void_p * len(peer_bufs))(*peer_bufs)
+        upd = None
+        if update is not None:
+            ents, wdt, lr, rescale, mom = update
+            arr = (_lib.UpdateEntry * max(1, len(ents)))(*[_lib.UpdateEntry(w, g, m or None, k) for w, g, m, k in ents])
+            u = _lib.P2PUpdateC(C.cast(arr, C.c_void_p), len(ents), wdt, lr, rescale, mom)
+            upd = C.byref(u)
+        check(lib.cs_allreduce_p2p(self.h, comm, rank, bufs, n, dtype, trace_key, upd, stream))
+
     def close(self):
         if self.h:
             lib.cs_transport_destroy(self.h)
@@ -350,6 +373,7 @@ class KvConfig:
     bucket_bytes: int = 0
     issue_order: int = 0
     comm_priority: int = 0
+    p2p: int = 0
 
 
 @dataclass
@@ -370,7 +394,8 @@ class KvStore:
                  concom_comms: Sequence[int] = ()):
         cfg = _lib.KvConfigC(MODES[config.mode] if isinstance(config.mode, str) else config.mode,
                              config.outstanding, config.num_keys, config.comm_dtype,
-                             config.bucket_bytes, config.issue_order, config.comm_priority)
+                             config.bucket_bytes, config.issue_order, config.comm_priority,
+                             int(config.p2p))
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()
         check(lib.cs_kv_create(engine.h, transport.h, rank, C.byref(cfg), comms, len(concom_comms),
@@ -487,12 +512,12 @@ class SynthModel:
                  mode: str = "depcha", w_dtype: int = F32, g_dtype: int = F32, comm_dtype: int = F32,
                  bucket_bytes: int = 0, issue_order: int = 0, outstanding: int = 1, lr: float = 0.1,
                  rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
-                 backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0,
+                 backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0, p2p: bool = False,
                  host_source: bool = False, concom_comms: Sequence[int] = (),
                  ready_ms: Sequence[float] | None = None):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
-                                int(fused_update), comm_priority, int(host_source))
+                                int(fused_update), comm_priority, int(host_source), int(p2p))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()

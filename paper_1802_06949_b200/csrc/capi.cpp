@@ -3,8 +3,11 @@
 // nothing throws across the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "collsim_b200.h"
 #include "engine.hpp"
@@ -347,6 +350,67 @@ int cs_barrier(cs_transport_t t, int comm, int rank, int trace_key, cs_stream_t 
   });
 }
 
+int cs_transport_p2p_capable(cs_transport_t t, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *out = t->t->p2p_capable() ? 1 : 0;
+  });
+}
+int cs_transport_share_buffer(cs_transport_t t, void* base, void** ptrs_out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    std::vector<void*> p = t->t->share_buffer(base);
+    for (size_t i = 0; i < p.size(); ++i) ptrs_out[i] = p[i];
+  });
+}
+namespace {
+struct P2PTables {  // resident tables of the C-ABI p2p entry point, per stream
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, std::unique_ptr<DeviceTable>> by_stream;
+};
+P2PTables& p2p_tables() {
+  static P2PTables t;
+  return t;
+}
+}  // namespace
+int cs_allreduce_p2p(cs_transport_t t, int comm, int rank, void* const* peer_bufs, uint64_t n, cs_dtype dt,
+                     int trace_key, const cs_p2p_update* upd, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!upd) {
+      t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, nullptr);
+      return;
+    }
+    const size_t esz = dtype_size(dt);
+    const char* base = static_cast<const char*>(peer_bufs[rank]);
+    std::vector<DeviceTable::Entry> es;
+    for (int i = 0; i < upd->n_entries; ++i) {
+      const cs_update_entry& e = upd->entries[i];
+      const uint64_t off = static_cast<uint64_t>(static_cast<const char*>(e.g) - base) / esz;
+      if (off % 8 || off + e.n > n) throw UsageError("cs_allreduce_p2p: entry outside the bucket or misaligned");
+      es.push_back(DeviceTable::Entry{e.g, e.mom, e.w, e.n, off / 8, off / 8 + (e.n + 7) / 8});
+    }
+    std::sort(es.begin(), es.end(), [](const auto& x, const auto& y) { return x.gstart < y.gstart; });
+    DeviceTable* tab;
+    {
+      auto& reg = p2p_tables();
+      std::lock_guard<std::mutex> lock(reg.mu);
+      auto& p = reg.by_stream[s];
+      if (!p) p = std::make_unique<DeviceTable>();
+      tab = p.get();
+    }
+    Transport::P2PUpdate u;
+    u.tab = tab->resident(es, s);
+    u.n_entries = static_cast<int>(es.size());
+    u.wdt = upd->w_dtype;
+    u.lr = upd->lr;
+    u.rescale = upd->rescale;
+    u.momentum = upd->momentum;
+    t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, &u);
+  });
+}
+
 // ------------------------------------------------------------ kvstore
 int cs_create_communicators(cs_transport_t t, int count, int* comms_out) {
   return guard([&] {
@@ -370,6 +434,7 @@ int cs_kv_create(cs_engine_t e, cs_transport_t t, int rank, const cs_kv_config* 
     c.bucket_bytes = cfg->bucket_bytes;
     c.issue_order = cfg->issue_order;
     c.comm_priority = cfg->comm_priority;
+    c.p2p = cfg->p2p;
     std::vector<int> comms;
     for (int i = 0; i < n_comms; ++i) comms.push_back(concom_comms[i]);
     auto h = std::make_unique<cs_kvstore>();
@@ -482,6 +547,7 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     c.fused = cfg->fused_update != 0;
     c.comm_priority = cfg->comm_priority;
     c.host_source = cfg->host_source != 0;
+    c.p2p = cfg->p2p;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
@@ -515,6 +581,7 @@ int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nran
     c.fused = cfg->fused_update != 0;
     c.comm_priority = cfg->comm_priority;
     c.host_source = cfg->host_source != 0;
+    c.p2p = cfg->p2p;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);

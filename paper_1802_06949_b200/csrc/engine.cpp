@@ -63,7 +63,7 @@ Engine::Engine(int num_worker_threads, int rank, TraceSink* trace, int device)
     lanes_.push_back(s);
   }
   workers_.reserve(static_cast<size_t>(num_worker_threads));
-  for (int i = 0; i < num_worker_threads; ++i) workers_.emplace_back([this] { worker_loop(); });
+  for (int i = 0; i < num_worker_threads; ++i) workers_.emplace_back([this, i] { worker_loop(i); });
 }
 
 Engine::~Engine() {
@@ -441,13 +441,15 @@ void Engine::drain_inline() {
   }
 }
 
-// Workers spin on the ready counter for a short while before blocking: a
+// Worker 0 spins on the ready counter for a short while before blocking: a
 // blocked thread takes tens of microseconds to wake, and every DepCha /
 // ConCom collective is handed to the pool, so wake-up latency would
-// otherwise serialize into the step (CSB_ENGINE_SPIN_US, default 200).
-void Engine::worker_loop() {
+// otherwise serialize into the step (CSB_ENGINE_SPIN_US, default 1000).  The
+// other workers block at once, so N ranks x T workers never oversubscribe
+// the host cores (a rank's collectives become ready one at a time anyway).
+void Engine::worker_loop(int index) {
   for (;;) {
-    const auto spin_until = std::chrono::steady_clock::now() + spin_;
+    const auto spin_until = std::chrono::steady_clock::now() + (index == 0 ? spin_ : std::chrono::microseconds(0));
     while (ready_count_.load(std::memory_order_acquire) == 0 &&
            !stop_flag_.load(std::memory_order_relaxed) &&
            std::chrono::steady_clock::now() < spin_until) {

@@ -135,7 +135,7 @@ class Engine {
 
   OpId enqueue(std::unique_ptr<Operation> op, const std::vector<Tag>& reads,
                const std::vector<Tag>& mutates);
-  void worker_loop();
+  void worker_loop(int index);
   void run_op(Operation* op);         // no lock held
   void grant_head(VarRecord& var);    // mu_ held
   void decrement_pending(Operation* op);  // mu_ held
@@ -170,7 +170,7 @@ class Engine {
   std::atomic<int> ready_count_{0};
   std::atomic<bool> stop_flag_{false};
   int sleepers_ = 0;  // mu_
-  std::chrono::microseconds spin_{200};
+  std::chrono::microseconds spin_{1000};
 
   std::vector<cudaStream_t> lanes_;
   mutable std::mutex lanes_mu_;

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -517,6 +518,139 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ------------------------- fused NVLink allreduce (+ SGD) over peer memory
+//
+// One kernel per bucket per rank, all ranks launched with the same grid G
+// (cooperative launch, so every CTA is resident).  With T groups in the
+// bucket and N ranks, rank r owns shard r = groups [T*r/N, T*(r+1)/N); CTA
+// c owns chunk c of every shard (an even split over G).
+//   phase 1  CTA c of rank r reads chunk c of shard r from all N buckets
+//            (NVLink peer loads), adds them in rank order -- exactly the
+//            reference's ((b0 + b1) + b2) + ... (collective.cpp:229-233),
+//            so every rank ends with bit-identical sums -- and stores the
+//            sum into all N buckets (peer stores).
+//   phase 2  after CTA c of every rank has finished phase 1 (pairwise
+//            flags), CTA c runs the fused SGD / momentum update over chunk
+//            c of every shard, reading the reduced gradient from its LOCAL
+//            bucket (kernel (c), no separate launch, no copy-back).
+// Synchronisation is per CTA pair: CTA c on rank r only waits for CTA c on
+// the other ranks (st.release.sys / ld.acquire.sys on epoch-stamped flags
+// in each rank's flag region), so there is no grid-wide barrier.  The
+// matching ledger guarantees every rank launches the same op sequence.
+
+constexpr int kP2PMaxCtas = 1184;
+
+struct P2PParams {
+  void* bufs[CS_MAX_RANKS];
+  uint32_t* flags[CS_MAX_RANKS];
+  const DevEntry* tab;
+  uint64_t groups;
+  double step, mu;
+  int nranks, rank, n_entries;
+  uint32_t epoch;
+};
+
+__device__ __forceinline__ void flag_store(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t flag_load(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// phase: 0 = arrival (my bucket is packed), 1 = my shard sums are stored
+__device__ __forceinline__ void pair_barrier(const P2PParams& p, int phase) {
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < p.nranks) {
+    __threadfence_system();
+    const size_t slot = (static_cast<size_t>(phase) * CS_MAX_RANKS + p.rank) * kP2PMaxCtas + blockIdx.x;
+    flag_store(p.flags[t] + slot, p.epoch);
+    const uint32_t* mine =
+        p.flags[p.rank] + (static_cast<size_t>(phase) * CS_MAX_RANKS + t) * kP2PMaxCtas + blockIdx.x;
+    uint64_t t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (static_cast<int32_t>(flag_load(mine) - p.epoch) < 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 60000000000ull) __trap();  // a peer never arrived: fail loudly, never hang
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+}
+
+template <int CDT, int M>
+__device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
+  using Acc = typename AccOf<CDT, CDT>::T;
+  const int m = (M > 0) ? M : p.nranks;
+  for (uint64_t q = a + threadIdx.x; q < b; q += kThreads) {
+    const uint64_t i = q * kVec;
+    Acc acc[kVec];
+    if constexpr (M > 0) {
+      Acc x[M][kVec];
+#pragma unroll
+      for (int r = 0; r < M; ++r) load8_rw<CDT, Acc>(p.bufs[r], i, x[r]);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) acc[j] = x[0][j];
+#pragma unroll
+      for (int r = 1; r < M; ++r)
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[r][j]);
+#pragma unroll
+      for (int r = 0; r < M; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+    } else {
+      load8_rw<CDT, Acc>(p.bufs[0], i, acc);
+      for (int r = 1; r < m; ++r) {
+        Acc x[kVec];
+        load8_rw<CDT, Acc>(p.bufs[r], i, x);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[j]);
+      }
+      for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+    }
+  }
+}
+
+// SGD over bucket groups [a, b) through the entries (bucket-group coordinates)
+template <int WDT, int CDT, bool MOM>
+__device__ __forceinline__ void p2p_update_range(const P2PParams& p, uint64_t a, uint64_t b) {
+  if (a >= b || p.n_entries == 0) return;
+  int lo = 0, hi = p.n_entries;  // first entry with gend > a
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p.tab[mid].gend <= a) lo = mid + 1;
+    else hi = mid;
+  }
+  for (int e = lo; e < p.n_entries; ++e) {
+    const DevEntry en = p.tab[e];
+    if (en.gstart >= b) break;
+    const uint64_t s0 = max(a, en.gstart), s1 = min(b, en.gend);
+    const bool vec = ((reinterpret_cast<uintptr_t>(en.a) | reinterpret_cast<uintptr_t>(en.b) |
+                       reinterpret_cast<uintptr_t>(en.c)) & 15u) == 0;
+    sgd_segment<WDT, CDT, MOM>(en.c, en.a, const_cast<void*>(en.b), en.n, vec, s0 - en.gstart,
+                               s1 - en.gstart, p.step, p.mu);
+  }
+}
+
+template <int CDT, int WDT, bool UPDATE, bool MOM, int M>
+__global__ void __launch_bounds__(kThreads) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
+  const uint64_t T = p.groups;
+  const uint64_t G = gridDim.x, c = blockIdx.x;
+  pair_barrier(p, 0);
+  {
+    const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
+    p2p_reduce_chunk<CDT, M>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+  }
+  pair_barrier(p, 1);
+  if constexpr (UPDATE) {
+    for (int s = 0; s < p.nranks; ++s) {
+      const uint64_t s0 = T * s / p.nranks, s1 = T * (s + 1) / p.nranks, L = s1 - s0;
+      p2p_update_range<WDT, CDT, MOM>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+    }
+  }
+}
+
 // ------------------------------------------------- synthetic backward
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -649,12 +783,27 @@ int sm_count_for_current_device() {
 
 // One full wave: SMs x resident CTAs of this kernel (occupancy queried once
 // per instantiation), fewer when there is less than a group per thread.
+// CTAs per SM the streaming kernels may take.  Leaving part of every SM's
+// register file free lets a concurrently launched collective (NCCL's CTAs,
+// the cooperative peer kernel) start beside them instead of queueing behind
+// a full-occupancy wave; 3 x 256 threads per SM is also the measured optimum
+// of the standalone kernels (fewer CTAs contending for the L1tex queue).
+// CSB_STREAM_CTAS_PER_SM overrides (default 3).
+int stream_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = std::getenv("CSB_STREAM_CTAS_PER_SM");
+    const int x = e ? std::atoi(e) : 3;
+    return std::max(1, std::min(8, x));
+  }();
+  return v;
+}
+
 template <typename Kernel>
 int wave_grid(Kernel kernel, uint64_t groups) {
   static const int occ = [&] {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess) b = 1;
-    return std::max(1, b);
+    return std::max(1, std::min(b, stream_ctas_per_sm()));
   }();
   const uint64_t full = static_cast<uint64_t>(sm_count_for_current_device()) * occ;
   const uint64_t need = (groups + kThreads - 1) / kThreads;
@@ -1026,6 +1175,78 @@ void DeviceTable::sgd(const cs_update_entry* es, int n, int wdt, int gdt, double
 #undef CSB_SGD_TAB
   throw UsageError(std::string("cs_sgd_update: unsupported dtype pair w=") + dtype_name(wdt) +
                    " g=" + dtype_name(gdt));
+}
+
+const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cudaStream_t s) {
+  host_ = es;
+  vec_.assign(es.size(), 0);
+  groups_ = 0;
+  grid_ = 0;
+  first_.clear();
+  if (es.empty()) return nullptr;
+  sync(nullptr, s);
+  return static_cast<const Entry*>(dev_);
+}
+
+size_t p2p_flag_bytes() { return sizeof(uint32_t) * 2 * CS_MAX_RANKS * kP2PMaxCtas; }
+
+// The grid is a pure function of (groups, nranks): identical on every rank,
+// as the per-CTA pairing requires; <= 2 CTAs per SM so the cooperative launch
+// fits beside the other lanes' kernels.
+int p2p_grid(uint64_t groups, int nranks) {
+  const uint64_t per_rank = groups / static_cast<uint64_t>(nranks);
+  const uint64_t want = std::max<uint64_t>(1, per_rank / (2 * kThreads));
+  return static_cast<int>(std::min<uint64_t>(std::min<uint64_t>(want, 296), kP2PMaxCtas));
+}
+
+void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
+  if (a.nranks < 2 || a.nranks > CS_MAX_RANKS) throw UsageError("p2p_allreduce: 2 <= nranks <= 16");
+  if (a.count % kVec) throw UsageError("p2p_allreduce: bucket count must be a multiple of 8");
+  P2PParams p{};
+  for (int r = 0; r < a.nranks; ++r) {
+    p.bufs[r] = a.bufs[r];
+    p.flags[r] = a.flags[r];
+    if (!aligned16(a.bufs[r])) throw UsageError("p2p_allreduce: bucket not 16-byte aligned");
+  }
+  p.tab = a.tab;
+  p.n_entries = a.n_entries;
+  p.groups = a.count / kVec;
+  p.step = a.lr * a.rescale;  // model.cpp:21
+  p.mu = a.momentum;
+  p.nranks = a.nranks;
+  p.rank = a.rank;
+  p.epoch = a.epoch;
+  const int grid = p2p_grid(p.groups, a.nranks);
+  const bool upd = a.update && a.tab && a.n_entries > 0;
+  const bool mom = a.momentum != 0.0;
+  const double elems = static_cast<double>(a.count);
+  const double bytes = elems * dtype_size(a.cdt) * 2.0 / a.nranks * a.nranks +
+                       (upd ? elems * (dtype_size(a.cdt) + 2.0 * dtype_size(a.wdt) + (mom ? 8.0 : 0.0)) : 0.0);
+  LaunchScope ls(kKernSum, bytes, s);
+  void* args[] = {&p};
+  const void* fn = nullptr;
+#define CSB_P2P_PICK(C, W, U, MO)                                                                  \
+  if (a.cdt == C && (!U || a.wdt == W) && upd == U && (!U || mom == MO)) {                         \
+    switch (a.nranks) {                                                                            \
+      case 2: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 2>); break;     \
+      case 4: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 4>); break;     \
+      case 8: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 8>); break;     \
+      default: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 0>); break;    \
+    }                                                                                              \
+  }
+  CSB_P2P_PICK(CS_F32, CS_F32, false, false)
+  CSB_P2P_PICK(CS_BF16, CS_F32, false, false)
+  CSB_P2P_PICK(CS_F64, CS_F64, false, false)
+  CSB_P2P_PICK(CS_F32, CS_F32, true, false)
+  CSB_P2P_PICK(CS_F32, CS_F32, true, true)
+  CSB_P2P_PICK(CS_BF16, CS_F32, true, false)
+  CSB_P2P_PICK(CS_BF16, CS_F32, true, true)
+  CSB_P2P_PICK(CS_F64, CS_F64, true, false)
+  CSB_P2P_PICK(CS_F64, CS_F64, true, true)
+#undef CSB_P2P_PICK
+  if (!fn) throw UsageError("p2p_allreduce: unsupported dtype combination");
+  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, s));
+  ls.done();
 }
 
 uint64_t launch_count() { return g_launches.load(); }

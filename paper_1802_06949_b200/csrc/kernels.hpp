@@ -43,6 +43,8 @@ class DeviceTable {
     uint64_t n;
     uint64_t gstart, gend;
   };
+  // Keeps `es` resident (uploading on change) and returns the device copy.
+  const Entry* resident(const std::vector<Entry>& es, cudaStream_t s);
 
  private:
   void sync(const void* kernel, cudaStream_t s);
@@ -56,6 +58,26 @@ class DeviceTable {
   std::vector<unsigned char> shadow_;  // what dev_ holds
   uint64_t uploads_ = 0;
 };
+
+// Fused allreduce (+ SGD) over NVLink peer memory (kernels.cu): `bufs` /
+// `flags` hold every rank's bucket base and flag region (UVA / IPC-mapped),
+// `tab` the update entries in bucket-group coordinates (gstart = slot offset
+// / 8), sorted; nullptr / update=false reduces only.
+struct P2PArgs {
+  void* bufs[CS_MAX_RANKS];
+  uint32_t* flags[CS_MAX_RANKS];
+  int nranks = 0, rank = 0;
+  uint64_t count = 0;  // bucket elements, multiple of 8
+  int cdt = CS_F32, wdt = CS_F32;
+  uint32_t epoch = 0;  // identical on every rank for the same op (ledger seq + 1)
+  const DeviceTable::Entry* tab = nullptr;
+  int n_entries = 0;
+  bool update = false;
+  double lr = 0, rescale = 0, momentum = 0;
+};
+size_t p2p_flag_bytes();
+int p2p_grid(uint64_t groups, int nranks);
+void p2p_allreduce(const P2PArgs& args, cudaStream_t s);
 
 // Launch accounting and optional per-launch CUDA-event timing (roofline).
 enum KernelKind { kKernPack = 0, kKernSum = 1, kKernSgd = 2, kKernSynth = 3, kKernChecksum = 4, kKernKinds = 5 };

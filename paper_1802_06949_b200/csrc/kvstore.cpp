@@ -7,6 +7,7 @@
 #include "kvstore.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "hostprof.hpp"
@@ -64,6 +65,15 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   }
   if (cfg_.comm_dtype >= 0) dtype_size(cfg_.comm_dtype);  // validates
   comm_dt_ = cfg_.comm_dtype;
+  if (cfg_.p2p && cfg_.bucket_bytes == 0)
+    throw ConfigError("KvStore: the peer-memory path needs fusion buckets (bucket_bytes > 0)");
+  // Peer kernels pair CTAs across GPUs and are cooperative-launched; two of
+  // them on concurrent streams of one GPU (ConCom's communicators) could each
+  // hold the SMs the other needs on a peer, so ConCom stays on NCCL.
+  if (cfg_.p2p && cfg_.mode == KvMode::ConCom)
+    throw ConfigError("KvStore: the peer-memory path runs on one ordered comm stream (funnel/depcha)");
+  // one rank: nothing crosses NVLink, the collectives are the identity
+  p2p_active_ = cfg_.p2p != 0 && transport_.p2p_capable();
   if (engine_.device() < 0) throw ConfigError("KvStore: the engine must be bound to a CUDA device");
   keys_.resize(static_cast<size_t>(cfg_.num_keys));
   init_order_tag_ = engine_.new_variable();
@@ -228,6 +238,14 @@ void KvStore::build_buckets() {
       b.lane = world_lane_;
     }
   }
+  if (p2p_active_) {
+    // setup-phase collective: every rank maps every peer's arena (CUDA IPC)
+    const std::vector<void*> peers = transport_.share_buffer(arena);
+    for (Bucket& b : bs) {
+      const uint64_t boff = static_cast<uint64_t>(static_cast<char*>(b.base) - arena);
+      for (void* p : peers) b.peer_bufs.push_back(static_cast<char*>(p) + boff);
+    }
+  }
   buckets_ = std::move(bs);
   built_ = true;
 }
@@ -305,22 +323,28 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
   const int comm = B.comm;
   const int dt = comm_dt_;
   B.issued = true;
+  (void)tr;
+  (void)base;
+  (void)count;
+  (void)dt;
+  (void)comm;
+  (void)rank;
+  (void)key0;
+  (void)bid;
+  KvStore* self = this;
   if (cfg_.mode == KvMode::Funnel) {
     // control-thread collective on the single ordered comm stream
     // (kvstore.cpp:112-116); the funnel tag keeps issue order = push order
     muts.push_back(funnel_tag_);
-    engine_.push_stream(
-        [tr, rank, base, count, dt, key0, bid](cudaStream_t s) {
-          tr->allreduce_sum(Transport::world(), rank, base, count, dt, key0, s, bid);
-        },
-        {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+    engine_.push_stream([self, b](cudaStream_t s) { self->collective_body(self->buckets_[b], b, s, nullptr); },
+                        {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
   } else {
     // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136)
     std::atomic<int>* outstanding = &outstanding_;
     outstanding_.fetch_add(1);
     std::vector<Tag> reads = extra_reads;
     engine_.push_stream(
-        [tr, outstanding, comm, rank, base, count, dt, key0, bid](cudaStream_t s) {
+        [self, b, outstanding](cudaStream_t s) {
           struct Drain {
             std::atomic<int>* c;
             ~Drain() {
@@ -328,9 +352,30 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
               c->notify_all();
             }
           } drain{outstanding};
-          tr->allreduce_sum(comm, rank, base, count, dt, key0, s, bid);
+          self->collective_body(self->buckets_[b], b, s, nullptr);
         },
         reads, muts, OpKind::Collective, key0, B.lane, Dispatch::Pool);
+  }
+}
+
+Dispatch KvStore::depcha_dispatch() const {
+  static const bool pool = [] {
+    const char* e = std::getenv("CSB_DEPCHA_DISPATCH");
+    return e && std::string(e) == "pool";
+  }();
+  if (cfg_.mode == KvMode::Naive || pool) return Dispatch::Pool;
+  return Dispatch::Inline;
+}
+
+// One bucket's allreduce on its communicator: NCCL (or the local rank-order
+// kernel) by default, the peer-memory kernel when p2p is active (optionally
+// fused with the update of the keys in `upd`).
+void KvStore::collective_body(const Bucket& B, int b, cudaStream_t s, const Transport::P2PUpdate* upd) {
+  const int bid = cfg_.bucket_bytes ? b : -1;
+  if (p2p_active_) {
+    transport_.allreduce_p2p(B.comm, rank_, B.peer_bufs.data(), B.count, comm_dt_, B.keys[0], s, bid, upd);
+  } else {
+    transport_.allreduce_sum(B.comm, rank_, B.base, B.count, comm_dt_, B.keys[0], s, bid);
   }
 }
 
@@ -414,18 +459,48 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       // the copy-out / update follows as an op on the update lane.
       std::vector<Tag> muts{B.tag};
       if (cfg_.mode == KvMode::DepCha) muts.push_back(dummy_tag_);
-      Transport* tr = &transport_;
-      const int rank = rank_;
-      void* base = B.base;
-      const uint64_t count = B.count;
       const int ckey = B.keys[0];
-      const int bid = cfg_.bucket_bytes ? b : -1;
       B.issued = true;
-      engine_.push_stream(
-          [tr, rank, base, count, cdt, ckey, bid](cudaStream_t s) {
-            tr->allreduce_sum(Transport::world(), rank, base, count, cdt, ckey, s, bid);
-          },
-          {}, muts, OpKind::Collective, ckey, B.lane, Dispatch::Pool);
+      KvStore* self = this;
+      const int bi = b;
+      if (p2p_active_ && upd) {
+        // peer-memory path: ONE kernel does the NVLink allreduce of the
+        // bucket and the SGD / momentum update of these keys (phase 2 reads
+        // the reduced gradient from the local bucket), mutating the weights
+        std::vector<DeviceTable::Entry> es;
+        for (size_t j = 0; j < updates.size(); ++j) {
+          const KeyState& ks = keys_[static_cast<size_t>(keys[static_cast<size_t>(idxs[j])])];
+          const uint64_t g0 = ks.offset / 8;
+          es.push_back(DeviceTable::Entry{updates[j].g, updates[j].mom, updates[j].w, updates[j].n, g0,
+                                          g0 + (updates[j].n + 7) / 8});
+        }
+        std::sort(es.begin(), es.end(), [](const auto& x, const auto& y) { return x.gstart < y.gstart; });
+        if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
+        DeviceTable* ptab = B.p2p_tab.get();  // all its uploads on B.lane
+        for (const Tag& t : out_tags) muts.push_back(t);
+        engine_.push_stream(
+            [self, bi, es, ptab, out_dt, opt](cudaStream_t s) {
+              Transport::P2PUpdate u;
+              u.tab = ptab->resident(es, s);
+              u.n_entries = static_cast<int>(es.size());
+              u.wdt = out_dt;
+              u.lr = opt.lr;
+              u.rescale = opt.rescale;
+              u.momentum = opt.momentum;
+              self->collective_body(self->buckets_[bi], bi, s, &u);
+            },
+            {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
+        for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;
+        B.pulled += static_cast<int>(idxs.size());
+        if (B.pulled == static_cast<int>(B.keys.size())) {
+          B.pushed = 0;
+          B.pulled = 0;
+          B.issued = false;
+        }
+        continue;
+      }
+      engine_.push_stream([self, bi](cudaStream_t s) { self->collective_body(self->buckets_[bi], bi, s, nullptr); },
+                          {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
     }
     engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
                         update_lane_, Dispatch::Inline);

@@ -43,6 +43,10 @@ struct KvConfig {
   uint64_t bucket_bytes = 0;  // 0: one buffer per key (reference map)
   int issue_order = 0;        // bucket grouping order: 0 ascending, 1 descending
   int comm_priority = 0;      // CUDA stream priority of the comm lanes
+  // Peer-memory collectives over NVLink instead of NCCL (needs fusion
+  // buckets and a peer-capable NCCL transport): bit-exact rank-order sums,
+  // and DepCha's pull_update becomes ONE fused allreduce+update kernel.
+  int p2p = 0;
 };
 
 // Non-owning device view + engine tag (kvstore.hpp:16-19).
@@ -111,7 +115,8 @@ class KvStore {
     int comm = 0;
     int lane = 0;
     Tag tag;  // engine tag of the whole comm buffer
-    std::shared_ptr<DeviceTable> pack_tab, upd_tab, unpack_tab;  // resident kernel tables
+    std::shared_ptr<DeviceTable> pack_tab, upd_tab, unpack_tab, p2p_tab;  // resident kernel tables
+    std::vector<void*> peer_bufs;  // p2p: this bucket on every rank (IPC-mapped)
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -122,6 +127,13 @@ class KvStore {
                  const SgdConfig* sgd);
   void* key_ptr(int key) const;
   void ensure_momentum(int key, int wdt);
+  bool use_p2p() const { return p2p_active_; }
+  // DepCha collectives: the dummy tag already fixes their order, so they can
+  // be dispatched by the granting thread (no pool hand-off per collective);
+  // naive keeps the pool (its hazard comes from racing pool threads).
+  // CSB_DEPCHA_DISPATCH=pool restores the reference's pool dispatch.
+  Dispatch depcha_dispatch() const;
+  void collective_body(const Bucket& B, int bucket_id, cudaStream_t s, const Transport::P2PUpdate* upd);
 
   Engine& engine_;
   Transport& transport_;
@@ -141,6 +153,7 @@ class KvStore {
   Tag funnel_tag_;
   int initialized_count_ = 0;
   bool built_ = false;
+  bool p2p_active_ = false;
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call
   uint32_t stamp_ = 0;
   uint32_t next_stamp() {

@@ -48,6 +48,8 @@ std::string describe_call(const CallSig& sig);
 constexpr int kLedgerMaxRanks = 16;
 constexpr int kLedgerMaxComms = 17;  // world + up to 16 extra communicators
 constexpr int kLedgerSlots = 256;    // ring of in-flight sequence indices per comm
+constexpr int kLedgerRankBlobSlots = 64;  // per-rank setup mailbox slots
+constexpr int kRankBlobLen = 80;          // >= sizeof(cudaIpcMemHandle_t) + metadata
 
 struct LedgerShared;  // layout in ledger.cpp
 
@@ -105,6 +107,9 @@ class Ledger {
   // Setup mailbox for NCCL unique ids (shm mode): rank 0 posts, others wait.
   void post_blob(int index, const void* data, size_t n);
   void read_blob(int index, void* data, size_t n);
+  // Per-rank setup mailbox (CUDA IPC handles of peer-shared buffers).
+  void post_rank_blob(int slot, int rank, const void* data, size_t n);
+  void read_rank_blob(int slot, int rank, void* data, size_t n);
 
   uint64_t slot_uid(const Ticket& t) const { return static_cast<uint64_t>(t.comm) * kLedgerSlots + t.slot; }
 

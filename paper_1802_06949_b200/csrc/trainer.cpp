@@ -66,6 +66,7 @@ KvConfig kv_config(const SynthConfig& c) {
   k.bucket_bytes = c.bucket_bytes;
   k.issue_order = c.issue_order;
   k.comm_priority = c.comm_priority;
+  k.p2p = c.p2p;
   return k;
 }
 

@@ -35,6 +35,7 @@ struct SynthConfig {
   bool fused = true;         // pull_update (kernel (c) on the reduced bucket)
   int comm_priority = 0;
   bool host_source = false;  // gradients arrive from pinned host memory (e2e)
+  int p2p = 0;               // NVLink peer-memory collectives (KvConfig::p2p)
   uint64_t seed_base = 1000;
   // Measured gradient-ready time of every key from the start of a real
   // backward (tools/calibrate_backward.py).  When set, producers run in

@@ -114,13 +114,114 @@ std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int n
   ncclComm_t world = nullptr;
   CSB_NCCL(ncclCommInitRank(&world, nranks, id, rank), nullptr);
   t->comms_.push_back(world);
+  if (nranks > 1) {
+    int ndev = 0;
+    CSB_CUDA(cudaGetDeviceCount(&ndev));
+    bool ok = ndev >= nranks;
+    for (int d = 0; ok && d < ndev; ++d) {
+      if (d == device) continue;
+      int can = 0;
+      CSB_CUDA(cudaDeviceCanAccessPeer(&can, device, d));
+      ok = ok && can;
+    }
+    // every rank must agree, or the shared setup below would not match
+    const int32_t mine = ok ? 1 : 0;
+    t->ledger_->post_rank_blob(kLedgerRankBlobSlots - 1, rank, &mine, sizeof(mine));
+    for (int r = 0; r < nranks; ++r) {
+      int32_t v = 0;
+      t->ledger_->read_rank_blob(kLedgerRankBlobSlots - 1, r, &v, sizeof(v));
+      ok = ok && v;
+    }
+    t->p2p_ok_ = ok;
+    if (ok) t->setup_flags();
+  }
   return t;
+}
+
+std::vector<void*> Transport::share_buffer(void* base) {
+  if (!p2p_capable()) throw UsageError("Transport: peer-memory path needs the NCCL backend on peer-capable GPUs");
+  std::lock_guard<std::mutex> lock(mu_);
+  if (share_slots_ >= kLedgerRankBlobSlots - 1) throw ConfigError("Transport: too many shared buffers");
+  const int slot = share_slots_++;
+  CSB_CUDA(cudaSetDevice(device_));
+  cudaIpcMemHandle_t h;
+  CSB_CUDA(cudaIpcGetMemHandle(&h, base));
+  static_assert(sizeof(cudaIpcMemHandle_t) <= kRankBlobLen, "IPC handle does not fit the mailbox");
+  ledger_->post_rank_blob(slot, rank_, &h, sizeof(h));
+  std::vector<void*> ptrs(static_cast<size_t>(num_ranks()), nullptr);
+  for (int r = 0; r < num_ranks(); ++r) {
+    if (r == rank_) {
+      ptrs[r] = base;
+      continue;
+    }
+    cudaIpcMemHandle_t ph;
+    ledger_->read_rank_blob(slot, r, &ph, sizeof(ph));
+    void* p = nullptr;
+    CSB_CUDA(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
+    ipc_opened_.push_back(p);
+    ptrs[r] = p;
+  }
+  return ptrs;
+}
+
+void Transport::setup_flags() {
+  void* f = nullptr;
+  CSB_CUDA(cudaSetDevice(device_));
+  CSB_CUDA(cudaMalloc(&f, p2p_flag_bytes()));
+  CSB_CUDA(cudaMemset(f, 0, p2p_flag_bytes()));
+  CSB_CUDA(cudaDeviceSynchronize());
+  own_flags_.push_back(f);
+  flags_.push_back(share_buffer(f));
+}
+
+void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
+                              int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd) {
+  if (!p2p_capable()) throw UsageError("Transport: peer-memory path unavailable");
+  if (count == 0) throw UsageError("allreduce_sum: empty buffer");
+  CallSig sig;
+  sig.kind = CollKind::AllreduceSum;
+  sig.dtype = dtype;
+  sig.count = static_cast<int64_t>(count);
+  Ledger::Ticket t;
+  {
+    hostprof::Scope prof(hostprof::kLedger);
+    t = ledger_->arrive(comm, rank, sig, trace_key, bucket);
+  }
+  if (t.last) ledger_->finish(t);
+  P2PArgs a;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (comm < 0 || comm >= static_cast<int>(flags_.size())) throw UsageError("collective: unknown communicator");
+    for (int r = 0; r < num_ranks(); ++r) {
+      a.bufs[r] = peer_bufs[r];
+      a.flags[r] = static_cast<uint32_t*>(flags_[static_cast<size_t>(comm)][static_cast<size_t>(r)]);
+    }
+  }
+  a.nranks = num_ranks();
+  a.rank = rank;
+  a.count = count;
+  a.cdt = dtype;
+  a.epoch = static_cast<uint32_t>(t.seq + 1);  // same matched sequence on every rank
+  if (upd) {
+    a.update = true;
+    a.tab = upd->tab;
+    a.n_entries = upd->n_entries;
+    a.wdt = upd->wdt;
+    a.lr = upd->lr;
+    a.rescale = upd->rescale;
+    a.momentum = upd->momentum;
+  }
+  device_latency(stream);
+  p2p_allreduce(a, stream);
+  ledger_->depart(t, trace_key, bucket);
 }
 
 Transport::~Transport() {
   if (backend_ == Backend::Nccl) {
     const bool aborted = ledger_ && ledger_->latched();
     cudaSetDevice(device_);
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (void* p : own_flags_) cudaFree(p);
     for (ncclComm_t c : comms_) {
       if (!c) continue;
       if (aborted) ncclCommAbort(c);
@@ -139,6 +240,7 @@ int Transport::new_communicator() {
     if (static_cast<int>(comms_.size()) != id) throw UsageError("Transport: communicator ids diverged");
     comms_.push_back(c);
   }
+  if (p2p_capable()) setup_flags();  // every comm gets its own flag region
   return id;
 }
 

@@ -28,6 +28,7 @@
 #include <string>
 #include <vector>
 
+#include "kernels.hpp"
 #include "ledger.hpp"
 
 namespace csb {
@@ -64,6 +65,25 @@ class Transport {
   void abort(const std::string& why);
   Ledger& ledger() { return *ledger_; }
 
+  // ---- peer-memory path (one process per GPU, NVLink) --------------------
+  // True for the NCCL backend with >= 2 ranks on peer-capable devices.
+  bool p2p_capable() const { return backend_ == Backend::Nccl && num_ranks() > 1 && p2p_ok_; }
+  // Setup-phase collective: every rank passes the base of one cudaMalloc
+  // allocation, in the same order; returns every rank's mapping of its peer
+  // (CUDA IPC handles exchanged through the ledger), own entry = base.
+  std::vector<void*> share_buffer(void* base);
+  struct P2PUpdate {
+    const DeviceTable::Entry* tab = nullptr;  // bucket-group coordinates, sorted
+    int n_entries = 0;
+    int wdt = CS_F32;
+    double lr = 0, rescale = 0, momentum = 0;
+  };
+  // Allreduce of one bucket through peer memory, matched by the ledger like
+  // allreduce_sum; with `upd`, fused with the SGD / momentum update of the
+  // keys in the bucket (kernels.cu p2p_allreduce_kernel).
+  void allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
+                     int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd);
+
  private:
   Transport() = default;
   struct SlotDev;  // per (comm, ring slot) payload of the local backend
@@ -80,6 +100,13 @@ class Transport {
   std::vector<ncclComm_t> comms_;  // nccl: index = communicator id
   std::vector<std::unique_ptr<SlotDev>> slots_;  // local: comm * kLedgerSlots + slot
   std::mutex mu_;
+  // peer-memory path
+  void setup_flags();  // one flag region per communicator, shared
+  bool p2p_ok_ = false;
+  int share_slots_ = 0;
+  std::vector<void*> ipc_opened_;
+  std::vector<void*> own_flags_;
+  std::vector<std::vector<void*>> flags_;  // comm -> every rank's flag region
 };
 
 }  // namespace csb

@@ -60,14 +60,18 @@ def main():
         eng.wait_all()
         np.savez(outdir / f"{case}_r{rank}.npz", *[x.cpu().numpy() for x in res])
         eng.close()
-    elif case in ("funnel", "depcha", "concom"):
+    elif case.split("_")[0] in ("funnel", "depcha", "concom"):
+        mode = case.split("_")[0]
+        p2p = case.endswith("_p2p")
         gold = np.load(HERE / "golden" / "train_steps.npz")
         sizes = [int(x) for x in gold["sizes"]]
         K, lr, rescale = len(sizes), float(gold["lr"]), 1.0 / (64 * world)
-        outstanding = 2 if case == "concom" else 1
-        comms = create_communicators(tr, outstanding) if case == "concom" else []
+        outstanding = 2 if mode == "concom" else 1
+        comms = create_communicators(tr, outstanding) if mode == "concom" else []
         eng = Engine(4, rank, sink, local)
-        store = KvStore(eng, tr, rank, KvConfig(case, outstanding, K), comms)
+        cfg = KvConfig(mode, outstanding, K, bucket_bytes=16 * 1024 if p2p else 0, p2p=int(p2p))
+        store = KvStore(eng, tr, rank, cfg, comms)
+        case_mode = mode
         ws = [Slot(t64(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n), dev),
                    eng.new_variable()) for k, n in enumerate(sizes)]
         gs = [Slot(t64(O.random_uniform(n, 1000 + rank * K + k), dev), eng.new_variable())
@@ -81,7 +85,7 @@ def main():
                 sp, dp, n = src[k].data_ptr(), gs[k].value.data_ptr(), sizes[k]
                 eng.push_stream(lambda st, sp=sp, dp=dp, n=n: api.synth_backward(sp, dp, n, api.F64, 0, 0, st),
                                 [], [gs[k].tag], api.COMPUTE, k)
-            if case == "depcha":
+            if case_mode == "depcha":
                 store.push(list(range(K)), gs)
                 store.pull_update(list(range(K)), ws, lr, rescale)
             else:
@@ -89,12 +93,12 @@ def main():
                 for k in range(K):
                     store.push(k, gs[k])
                     store.pull_update(k, ws[k], lr, rescale)
-                    if case == "concom":
+                    if case_mode == "concom":
                         since += 1
                         if since == outstanding:
                             store.barrier()
                             since = 0
-                if case == "concom" and since:
+                if case_mode == "concom" and since:
                     store.barrier()
             eng.wait_all()
         np.savez(outdir / f"{case}_r{rank}.npz", *[w.value.cpu().numpy() for w in ws])
@@ -126,7 +130,7 @@ def main():
     else:
         raise SystemExit(f"unknown case {case}")
 
-    if case in ("funnel", "depcha", "concom"):
+    if case.split("_")[0] in ("funnel", "depcha", "concom"):
         out["trace"] = [f"{e['kind']}:{e['comm']}:{e['seq']}:{e.get('key', -1)}"
                         for e in sink.snapshot() if e["event"] == "coll_enqueued"]
     (outdir / f"{case}_r{rank}.json").write_text(json.dumps(out))
