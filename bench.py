@@ -44,7 +44,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "aggregated gradient GB/s/GPU & exposed comm ms/iter at 1/2/4/8 B200"
 CONFIGS = {
     # name: (keyset, mode, outstanding, dtype, bucket_mb, backward calibration or fixed ms)
-    "resnet50": ("resnet50", "depcha", 1, "fp32", 25, "resnet50_b64.json"),
+    "resnet50": ("resnet50", "depcha", 1, "fp32", 50, "resnet50_b64.json"),
     "alexnet": ("alexnet", "concom", 4, "fp32", 25, "alexnet_b64_amp.json"),
     "resnet152": ("resnet152", "depcha", 1, "bf16", 25, "resnet152_b64_amp.json"),
     "inception_v3": ("inception_v3", "depcha", 1, "bf16", 25, 30.0),
@@ -83,7 +83,7 @@ def parse():
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
-    p.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+    p.add_argument("--comm", default="nccl", choices=["nccl", "p2p", "nvls"],
                    help="collective engine for N>1: NCCL, or the fused NVLink peer-memory kernel")
     return p.parse_args()
 
@@ -106,13 +106,15 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
+    def __init__(self, devices: str, enabled: bool = True):
+        self.device = devices  # "0" or "0,1,2,3": one process samples every GPU of the job
+        self.ndev = len(devices.split(","))
         self.rows = []
         self.proc = None
+        self.enabled = enabled
 
     def __enter__(self):
-        if os.environ.get("CSB_CLOCKS") == "off":
+        if os.environ.get("CSB_CLOCKS") == "off" or not self.enabled:
             return self
         try:
             self.proc = subprocess.Popen(
@@ -129,7 +131,7 @@ class Clocks:
         ~200 ms away)."""
         t0 = time.time()
         n0 = len(self.rows)
-        while self.proc and len(self.rows) <= max(n0, 0) and time.time() - t0 < timeout:
+        while self.proc and len(self.rows) < n0 + self.ndev and time.time() - t0 < timeout:
             time.sleep(0.001)
 
     def _read(self):
@@ -266,9 +268,12 @@ def main():
     common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
-                  backward_ns=int(bwd_ms * 1e6), comm_priority=-5, p2p=args.comm == "p2p")
-    config["collectives"] = "fused NVLink peer-memory allreduce+update" if (args.comm == "p2p" and world > 1) \
-        else ("NCCL" if world > 1 else "identity (1 rank)")
+                  backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
+                  p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm])
+    config["collectives"] = ("identity (1 rank)" if world == 1 else
+                             {"nccl": "NCCL",
+                              "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
+                              "nvls": "fused allreduce+update kernel, NVSwitch multicast in-switch reduction"}[args.comm])
     model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, ready_ms=ready_ms,
                            **common)
     model.init()
@@ -283,7 +288,8 @@ def main():
     barrier()
     api.host_profile(reset=True)
     l0 = api.launch_count()
-    with Clocks(local_rank) as clk:
+    with Clocks(",".join(str(d) for d in range(world)) if world > 1 else str(local_rank),
+                enabled=(rank == 0)) as clk:
         clk.wait_first()
         clk.wait_first()  # aligned to the sampler's period, not its start-up
         barrier()

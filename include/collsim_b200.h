@@ -173,9 +173,20 @@ typedef struct cs_p2p_update {
   int n_entries;
   int w_dtype;
   double lr, rescale, momentum;
+  int shard_only; /* 1: on return the bucket holds only this rank's shard of the sum (the update
+                     read the other shards from their owners' buckets: less NVLink and HBM traffic);
+                     0: the whole sum, as without an update.  Ignored by cs_allreduce_nvls. */
 } cs_p2p_update;
 int cs_allreduce_p2p(cs_transport_t t, int comm, int rank, void* const* peer_bufs, uint64_t n,
                      cs_dtype dt, int trace_key, const cs_p2p_update* upd, cs_stream_t stream);
+/* NVLink SHARP: setup-phase collective allocating `bytes` bound to an NVSwitch
+ * multicast object on every rank; *uc = this rank's copy, *mc = multicast VA.
+ * cs_allreduce_nvls reduces in the switch (multimem.ld_reduce / multimem.st),
+ * optionally fused with the update as cs_allreduce_p2p (f32 / bf16). */
+int cs_transport_nvls_capable(cs_transport_t t, int* out);
+int cs_transport_alloc_nvls(cs_transport_t t, uint64_t bytes, void** uc, void** mc);
+int cs_allreduce_nvls(cs_transport_t t, int comm, int rank, void* uc, void* mc, uint64_t n, cs_dtype dt,
+                      int trace_key, const cs_p2p_update* upd, cs_stream_t stream);
 
 /* ----------------------------------------------------------- kvstore */
 typedef struct cs_kvstore* cs_kvstore_t;

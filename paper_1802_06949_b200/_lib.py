@@ -33,7 +33,7 @@ class UpdateEntry(C.Structure):
 
 class P2PUpdateC(C.Structure):
     _fields_ = [("entries", C.c_void_p), ("n_entries", C.c_int), ("w_dtype", C.c_int), ("lr", C.c_double),
-                ("rescale", C.c_double), ("momentum", C.c_double)]
+                ("rescale", C.c_double), ("momentum", C.c_double), ("shard_only", C.c_int)]
 
 
 class KvConfigC(C.Structure):
@@ -102,6 +102,9 @@ SIGNATURES = {
     "cs_transport_p2p_capable": [_P, _PI],
     "cs_transport_share_buffer": [_P, _P, C.POINTER(_P)],
     "cs_allreduce_p2p": [_P, _I, _I, C.POINTER(_P), _U64, _I, _I, C.c_void_p, _P],
+    "cs_transport_nvls_capable": [_P, _PI],
+    "cs_transport_alloc_nvls": [_P, _U64, C.POINTER(_P), C.POINTER(_P)],
+    "cs_allreduce_nvls": [_P, _I, _I, _P, _P, _U64, _I, _I, C.c_void_p, _P],
     "cs_create_communicators": [_P, _I, _PI],
     "cs_kv_create": [_P, _P, _I, C.POINTER(KvConfigC), _PI, _I, C.POINTER(_P)],
     "cs_kv_destroy": [_P],

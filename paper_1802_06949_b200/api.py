@@ -330,17 +330,37 @@ class Transport:
         check(lib.cs_transport_share_buffer(self.h, base, out))
         return [p or 0 for p in out]
 
+    @staticmethod
+    def _update_arg(update):
+        if update is None:
+            return None, None
+        ents, wdt, lr, rescale, mom, *rest = update
+        shard_only = int(bool(rest[0])) if rest else 0
+        arr = (_lib.UpdateEntry * max(1, len(ents)))(*[_lib.UpdateEntry(w, g, m or None, k) for w, g, m, k in ents])
+        u = _lib.P2PUpdateC(C.cast(arr, C.c_void_p), len(ents), wdt, lr, rescale, mom, shard_only)
+        return C.byref(u), (arr, u)
+
     def allreduce_p2p(self, comm: int, rank: int, peer_bufs, n: int, dtype: int, trace_key: int = -1,
                       update=None, stream: int = 0) -> None:
-        """update: (entries[(w, g, mom, n)], w_dtype, lr, rescale, momentum) or None."""
+        """update: (entries[(w, g, mom, n)], w_dtype, lr, rescale, momentum[, shard_only]) or None."""
         bufs = (C.c_void_p * len(peer_bufs))(*peer_bufs)
-        upd = None
-        if update is not None:
-            ents, wdt, lr, rescale, mom = update
-            arr = (_lib.UpdateEntry * max(1, len(ents)))(*[_lib.UpdateEntry(w, g, m or None, k) for w, g, m, k in ents])
-            u = _lib.P2PUpdateC(C.cast(arr, C.c_void_p), len(ents), wdt, lr, rescale, mom)
-            upd = C.byref(u)
+        upd, _keep = self._update_arg(update)
         check(lib.cs_allreduce_p2p(self.h, comm, rank, bufs, n, dtype, trace_key, upd, stream))
+
+    def nvls_capable(self) -> bool:
+        v = C.c_int()
+        check(lib.cs_transport_nvls_capable(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def alloc_nvls(self, nbytes: int) -> tuple[int, int]:
+        uc, mc = C.c_void_p(), C.c_void_p()
+        check(lib.cs_transport_alloc_nvls(self.h, nbytes, C.byref(uc), C.byref(mc)))
+        return uc.value, mc.value
+
+    def allreduce_nvls(self, comm: int, rank: int, uc: int, mc: int, n: int, dtype: int, trace_key: int = -1,
+                       update=None, stream: int = 0) -> None:
+        upd, _keep = self._update_arg(update)
+        check(lib.cs_allreduce_nvls(self.h, comm, rank, uc, mc, n, dtype, trace_key, upd, stream))
 
     def close(self):
         if self.h:

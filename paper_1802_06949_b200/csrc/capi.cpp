@@ -373,13 +373,45 @@ P2PTables& p2p_tables() {
   return t;
 }
 }  // namespace
+namespace {
+void p2p_call(cs_transport_t t, int comm, int rank, void* const* peer_bufs, void* mc, uint64_t n, cs_dtype dt,
+              int trace_key, const cs_p2p_update* upd, cs_stream_t stream);
+}
+int cs_transport_nvls_capable(cs_transport_t t, int* out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    *out = t->t->nvls_capable() ? 1 : 0;
+  });
+}
+int cs_transport_alloc_nvls(cs_transport_t t, uint64_t bytes, void** uc, void** mc) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    NvlsBuffer b = t->t->alloc_nvls(bytes);  // lives as long as the process (bench / tests)
+    *uc = b.uc;
+    *mc = b.mc;
+  });
+}
+int cs_allreduce_nvls(cs_transport_t t, int comm, int rank, void* uc, void* mc, uint64_t n, cs_dtype dt,
+                      int trace_key, const cs_p2p_update* upd, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    std::vector<void*> bufs(static_cast<size_t>(t->t->num_ranks()), nullptr);
+    bufs[static_cast<size_t>(rank)] = uc;
+    p2p_call(t, comm, rank, bufs.data(), mc, n, dt, trace_key, upd, stream);
+  });
+}
 int cs_allreduce_p2p(cs_transport_t t, int comm, int rank, void* const* peer_bufs, uint64_t n, cs_dtype dt,
                      int trace_key, const cs_p2p_update* upd, cs_stream_t stream) {
-  return guard([&] {
+  return guard([&] { p2p_call(t, comm, rank, peer_bufs, nullptr, n, dt, trace_key, upd, stream); });
+}
+namespace {
+void p2p_call(cs_transport_t t, int comm, int rank, void* const* peer_bufs, void* mc, uint64_t n, cs_dtype dt,
+              int trace_key, const cs_p2p_update* upd, cs_stream_t stream) {
+  {
     CHECK_HANDLE(t);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!upd) {
-      t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, nullptr);
+      t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, nullptr, mc);
       return;
     }
     const size_t esz = dtype_size(dt);
@@ -407,9 +439,11 @@ int cs_allreduce_p2p(cs_transport_t t, int comm, int rank, void* const* peer_buf
     u.lr = upd->lr;
     u.rescale = upd->rescale;
     u.momentum = upd->momentum;
-    t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, &u);
-  });
+    u.shard_only = upd->shard_only != 0;
+    t->t->allreduce_p2p(comm, rank, peer_bufs, n, dt, trace_key, s, -1, &u, mc);
+  }
 }
+}  // namespace
 
 // ------------------------------------------------------------ kvstore
 int cs_create_communicators(cs_transport_t t, int count, int* comms_out) {

@@ -411,9 +411,10 @@ __device__ __forceinline__ void sgd_elem(Acc& w, Acc g, Acc& m, Acc step, Acc mu
   }
 }
 
-template <int WDT, int GDT, bool MOM>
+template <int WDT, int GDT, bool MOM, int NT = kThreads>
 __device__ __forceinline__ void sgd_segment(void* w, const void* g, void* mom, uint64_t n, bool vec,
                                             uint64_t lo, uint64_t hi, double step_d, double mu_d) {
+  constexpr int kThreads = NT;  // block size of the caller (the peer kernel uses 512)
   using Acc = typename AccOf<WDT, WDT>::T;  // f64 weights -> f64 math, else f32
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
   constexpr int U = 2;
@@ -539,14 +540,21 @@ __global__ void __launch_bounds__(kThreads)
 // matching ledger guarantees every rank launches the same op sequence.
 
 constexpr int kP2PMaxCtas = 1184;
+// 512-thread CTAs, one per SM: the NVLink phases run on the first 256 threads
+// (more outstanding peer requests measured slower), the local HBM update phase
+// on all 512.
+constexpr int kP2PThreads = 512;
+constexpr int kP2PLinkThreads = 256;
 
 struct P2PParams {
   void* bufs[CS_MAX_RANKS];
   uint32_t* flags[CS_MAX_RANKS];
+  void* mc;  // NVLS: multicast VA of the bucket (bufs unused in phase 1)
+  void* recv[CS_MAX_RANKS];  // push mode: every rank's receive area (nranks slots of slot_groups)
   const DevEntry* tab;
-  uint64_t groups;
+  uint64_t groups, slot_groups;
   double step, mu;
-  int nranks, rank, n_entries;
+  int nranks, rank, n_entries, shard_only;
   uint32_t epoch;
 };
 
@@ -559,7 +567,8 @@ __device__ __forceinline__ uint32_t flag_load(const uint32_t* p) {
   return v;
 }
 
-// phase: 0 = arrival (my bucket is packed), 1 = my shard sums are stored
+// phase: 0 = arrival (my bucket is packed), 1 = my shard sums are stored,
+// 2 = (shard_only) my update finished reading the owners' buckets
 __device__ __forceinline__ void pair_barrier(const P2PParams& p, int phase) {
   __syncthreads();
   const int t = threadIdx.x;
@@ -584,7 +593,8 @@ template <int CDT, int M>
 __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
   using Acc = typename AccOf<CDT, CDT>::T;
   const int m = (M > 0) ? M : p.nranks;
-  for (uint64_t q = a + threadIdx.x; q < b; q += kThreads) {
+  if (threadIdx.x >= kP2PLinkThreads) return;
+  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
     const uint64_t i = q * kVec;
     Acc acc[kVec];
     if constexpr (M > 0) {
@@ -597,8 +607,12 @@ __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a,
       for (int r = 1; r < M; ++r)
 #pragma unroll
         for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[r][j]);
+      if (p.shard_only) {
+        store8<CDT, Acc>(p.bufs[p.rank], i, acc);
+      } else {
 #pragma unroll
-      for (int r = 0; r < M; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+        for (int r = 0; r < M; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+      }
     } else {
       load8_rw<CDT, Acc>(p.bufs[0], i, acc);
       for (int r = 1; r < m; ++r) {
@@ -607,14 +621,125 @@ __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a,
 #pragma unroll
         for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[j]);
       }
-      for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+      if (p.shard_only) store8<CDT, Acc>(p.bufs[p.rank], i, acc);
+      else
+        for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
     }
   }
 }
 
-// SGD over bucket groups [a, b) through the entries (bucket-group coordinates)
+// NVLS phase 1: the NVSwitch sums every rank's copy (multimem.ld_reduce on the
+// multicast VA) and multimem.st writes the sum into every rank's copy.  The
+// switch's reduction order is not the reference's rank order, so this path is
+// within tolerance, not bit-exact (the IPC path above is bit-exact).
+template <int CDT>
+__device__ __forceinline__ void nvls_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
+  if (threadIdx.x >= kP2PLinkThreads) return;
+  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+    if constexpr (CDT == CS_F32) {
+      float* base = static_cast<float*>(p.mc) + q * kVec;
+      float v[8];
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(base) : "memory");
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "l"(base + 4) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                   ::"l"(base), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                   ::"l"(base + 4), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
+    } else {
+      __nv_bfloat16* base = static_cast<__nv_bfloat16*>(p.mc) + q * kVec;
+      uint32_t v[4];
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(base) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};"
+                   ::"l"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+    }
+  }
+}
+
+// Push mode, phase 0: CTA c copies chunk c of every peer's shard out of the
+// local bucket into slot `rank` of that peer's receive area -- NVLink carries
+// only posted writes (no remote-read round trips).  Destinations are staggered
+// (rank+1, rank+2, ...) so the N senders spread over the N receivers.
+template <int CDT>
+__device__ __forceinline__ void p2p_push_chunks(const P2PParams& p) {
+  constexpr uint64_t kGroupBytes = kVec * (CDT == CS_F64 ? 8 : CDT == CS_F32 ? 4 : 2);
+  const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
+  for (int k = 1; k < p.nranks; ++k) {
+    const int s = (p.rank + k) % p.nranks;
+    const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
+    const uint64_t a = s0 + L * c / G, b = s0 + L * (c + 1) / G;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(p.bufs[p.rank]) + a * kGroupBytes);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(p.recv[s]) +
+                                          (static_cast<uint64_t>(p.rank) * p.slot_groups + (a - s0)) * kGroupBytes);
+    const uint64_t n = (b - a) * (kGroupBytes / 16);
+    uint64_t i = threadIdx.x;
+    if (i >= kP2PLinkThreads) return;
+    for (; i + 3 * kP2PLinkThreads < n; i += 4 * kP2PLinkThreads) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = src[i + u * kP2PLinkThreads];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[i + u * kP2PLinkThreads] = v[u];
+    }
+    for (; i < n; i += kP2PLinkThreads) dst[i] = src[i];
+  }
+}
+
+// Push mode, phase 1: every addend of my shard chunk is now local (slot r of
+// my receive area, or my own bucket for r == rank); sum in rank order and
+// write the result into every rank's bucket.
+template <int CDT, int M>
+__device__ __forceinline__ void p2p_push_reduce_chunk(const P2PParams& p, uint64_t s0, uint64_t a, uint64_t b) {
+  using Acc = typename AccOf<CDT, CDT>::T;
+  const int m = (M > 0) ? M : p.nranks;
+  if (threadIdx.x >= kP2PLinkThreads) return;
+  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+    const uint64_t i = q * kVec;
+    const uint64_t j = (q - s0) * kVec;
+    Acc acc[kVec];
+    if constexpr (M > 0) {
+      Acc x[M][kVec];
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        const bool own = (r == p.rank);
+        load8<CDT, Acc>(own ? p.bufs[r] : p.recv[p.rank],
+                        own ? i : static_cast<uint64_t>(r) * p.slot_groups * kVec + j, x[r]);
+      }
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) acc[v] = x[0][v];
+#pragma unroll
+      for (int r = 1; r < M; ++r)
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) acc[v] = add_rn(acc[v], x[r][v]);
+      if (p.shard_only) {
+        store8<CDT, Acc>(p.bufs[p.rank], i, acc);
+      } else {
+#pragma unroll
+        for (int r = 0; r < M; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+      }
+    } else {
+      for (int r = 0; r < m; ++r) {
+        Acc x[kVec];
+        const bool own = (r == p.rank);
+        load8<CDT, Acc>(own ? p.bufs[r] : p.recv[p.rank],
+                        own ? i : static_cast<uint64_t>(r) * p.slot_groups * kVec + j, x);
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) acc[v] = (r == 0) ? x[v] : add_rn(acc[v], x[v]);
+      }
+      if (p.shard_only) store8<CDT, Acc>(p.bufs[p.rank], i, acc);
+      else
+        for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
+    }
+  }
+}
+
+// SGD over bucket groups [a, b) of shard `owner` through the entries
+// (bucket-group coordinates).  shard_only: the reduced gradient of another
+// owner's shard is read from that owner's bucket over NVLink.
 template <int WDT, int CDT, bool MOM>
-__device__ __forceinline__ void p2p_update_range(const P2PParams& p, uint64_t a, uint64_t b) {
+__device__ __forceinline__ void p2p_update_range(const P2PParams& p, int owner, uint64_t a, uint64_t b) {
   if (a >= b || p.n_entries == 0) return;
   int lo = 0, hi = p.n_entries;  // first entry with gend > a
   while (lo < hi) {
@@ -628,26 +753,43 @@ __device__ __forceinline__ void p2p_update_range(const P2PParams& p, uint64_t a,
     const uint64_t s0 = max(a, en.gstart), s1 = min(b, en.gend);
     const bool vec = ((reinterpret_cast<uintptr_t>(en.a) | reinterpret_cast<uintptr_t>(en.b) |
                        reinterpret_cast<uintptr_t>(en.c)) & 15u) == 0;
-    sgd_segment<WDT, CDT, MOM>(en.c, en.a, const_cast<void*>(en.b), en.n, vec, s0 - en.gstart,
-                               s1 - en.gstart, p.step, p.mu);
+    const void* g = en.a;
+    if (p.shard_only && owner != p.rank)
+      g = static_cast<const char*>(p.bufs[owner]) +
+          (static_cast<const char*>(en.a) - static_cast<const char*>(p.bufs[p.rank]));
+    sgd_segment<WDT, CDT, MOM, kP2PThreads>(en.c, g, const_cast<void*>(en.b), en.n, vec, s0 - en.gstart,
+                                            s1 - en.gstart, p.step, p.mu);
   }
 }
 
-template <int CDT, int WDT, bool UPDATE, bool MOM, int M>
-__global__ void __launch_bounds__(kThreads) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
+template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false, bool PUSH = false>
+__global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
   const uint64_t T = p.groups;
   const uint64_t G = gridDim.x, c = blockIdx.x;
+  if constexpr (PUSH) p2p_push_chunks<CDT>(p);
   pair_barrier(p, 0);
   {
     const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
-    p2p_reduce_chunk<CDT, M>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+    if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+    else if constexpr (PUSH) p2p_push_reduce_chunk<CDT, M>(p, s0, s0 + L * c / G, s0 + L * (c + 1) / G);
+    else p2p_reduce_chunk<CDT, M>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+  }
+  auto update_shard = [&](int s) {
+    const uint64_t s0 = T * s / p.nranks, s1 = T * (s + 1) / p.nranks, L = s1 - s0;
+    p2p_update_range<WDT, CDT, MOM>(p, s, s0 + L * c / G, s0 + L * (c + 1) / G);
+  };
+  if constexpr (UPDATE && !NVLS) {
+    // this CTA just wrote its chunk of the own shard: update it before
+    // waiting for the peers (absorbs their skew)
+    __syncthreads();
+    update_shard(p.rank);
   }
   pair_barrier(p, 1);
   if constexpr (UPDATE) {
-    for (int s = 0; s < p.nranks; ++s) {
-      const uint64_t s0 = T * s / p.nranks, s1 = T * (s + 1) / p.nranks, L = s1 - s0;
-      p2p_update_range<WDT, CDT, MOM>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
-    }
+    // the other shards, staggered so the ranks start on different owners
+    for (int k = NVLS ? 0 : 1; k < p.nranks; ++k) update_shard((p.rank + k) % p.nranks);
+    // shard_only: owners may repack their buckets only after every reader is done
+    if (p.shard_only) pair_barrier(p, 2);
   }
 }
 
@@ -1188,15 +1330,24 @@ const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cu
   return static_cast<const Entry*>(dev_);
 }
 
-size_t p2p_flag_bytes() { return sizeof(uint32_t) * 2 * CS_MAX_RANKS * kP2PMaxCtas; }
+size_t p2p_flag_bytes() { return sizeof(uint32_t) * 3 * CS_MAX_RANKS * kP2PMaxCtas; }
+
+size_t p2p_recv_bytes(uint64_t count, int cdt, int nranks) {
+  const uint64_t slot_groups = (count / kVec + nranks - 1) / nranks;
+  return static_cast<size_t>(nranks) * slot_groups * kVec * dtype_size(cdt);
+}
 
 // The grid is a pure function of (groups, nranks): identical on every rank,
 // as the per-CTA pairing requires; <= 2 CTAs per SM so the cooperative launch
 // fits beside the other lanes' kernels.
 int p2p_grid(uint64_t groups, int nranks) {
+  static const uint64_t cap = [] {
+    const char* e = std::getenv("CSB_P2P_CTAS");  // identical on every rank (same environment)
+    return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 148);
+  }();
   const uint64_t per_rank = groups / static_cast<uint64_t>(nranks);
-  const uint64_t want = std::max<uint64_t>(1, per_rank / (2 * kThreads));
-  return static_cast<int>(std::min<uint64_t>(std::min<uint64_t>(want, 296), kP2PMaxCtas));
+  const uint64_t want = std::max<uint64_t>(1, per_rank / (2 * kP2PLinkThreads));
+  return static_cast<int>(std::min<uint64_t>(std::min<uint64_t>(want, cap), kP2PMaxCtas));
 }
 
 void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
@@ -1206,8 +1357,16 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   for (int r = 0; r < a.nranks; ++r) {
     p.bufs[r] = a.bufs[r];
     p.flags[r] = a.flags[r];
-    if (!aligned16(a.bufs[r])) throw UsageError("p2p_allreduce: bucket not 16-byte aligned");
+    if (!a.mc && !aligned16(a.bufs[r])) throw UsageError("p2p_allreduce: bucket not 16-byte aligned");
   }
+  p.mc = a.mc;
+  const bool push = !a.mc && a.recv[0];
+  for (int r = 0; push && r < a.nranks; ++r) {
+    p.recv[r] = a.recv[r];
+    if (!aligned16(a.recv[r])) throw UsageError("p2p_allreduce: receive area not 16-byte aligned");
+  }
+  p.slot_groups = (a.count / kVec + a.nranks - 1) / a.nranks;
+  if (a.mc && !aligned16(a.mc)) throw UsageError("p2p_allreduce: multicast bucket not 16-byte aligned");
   p.tab = a.tab;
   p.n_entries = a.n_entries;
   p.groups = a.count / kVec;
@@ -1216,6 +1375,7 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   p.nranks = a.nranks;
   p.rank = a.rank;
   p.epoch = a.epoch;
+  p.shard_only = (a.shard_only && a.update && !a.mc) ? 1 : 0;
   const int grid = p2p_grid(p.groups, a.nranks);
   const bool upd = a.update && a.tab && a.n_entries > 0;
   const bool mom = a.momentum != 0.0;
@@ -1244,8 +1404,43 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   CSB_P2P_PICK(CS_F64, CS_F64, true, false)
   CSB_P2P_PICK(CS_F64, CS_F64, true, true)
 #undef CSB_P2P_PICK
+  if (push) {  // writes-only NVLink traffic through the receive areas
+    fn = nullptr;
+#define CSB_PUSH_PICK(C, W, U, MO)                                                                  \
+  if (a.cdt == C && (!U || a.wdt == W) && upd == U && (!U || mom == MO)) {                          \
+    switch (a.nranks) {                                                                             \
+      case 2: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 2, false, true>); break;  \
+      case 4: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 4, false, true>); break;  \
+      case 8: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 8, false, true>); break;  \
+      default: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 0, false, true>); break; \
+    }                                                                                               \
+  }
+    CSB_PUSH_PICK(CS_F32, CS_F32, false, false)
+    CSB_PUSH_PICK(CS_BF16, CS_F32, false, false)
+    CSB_PUSH_PICK(CS_F64, CS_F64, false, false)
+    CSB_PUSH_PICK(CS_F32, CS_F32, true, false)
+    CSB_PUSH_PICK(CS_F32, CS_F32, true, true)
+    CSB_PUSH_PICK(CS_BF16, CS_F32, true, false)
+    CSB_PUSH_PICK(CS_BF16, CS_F32, true, true)
+    CSB_PUSH_PICK(CS_F64, CS_F64, true, false)
+    CSB_PUSH_PICK(CS_F64, CS_F64, true, true)
+#undef CSB_PUSH_PICK
+  }
+  if (a.mc) {  // in-switch reduction through the multicast VA
+    fn = nullptr;
+#define CSB_NVLS_PICK(C, W, U, MO)                                                                       \
+  if (a.cdt == C && (!U || a.wdt == W) && upd == U && (!U || mom == MO))                                 \
+    fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 0, true>);
+    CSB_NVLS_PICK(CS_F32, CS_F32, false, false)
+    CSB_NVLS_PICK(CS_BF16, CS_F32, false, false)
+    CSB_NVLS_PICK(CS_F32, CS_F32, true, false)
+    CSB_NVLS_PICK(CS_F32, CS_F32, true, true)
+    CSB_NVLS_PICK(CS_BF16, CS_F32, true, false)
+    CSB_NVLS_PICK(CS_BF16, CS_F32, true, true)
+#undef CSB_NVLS_PICK
+  }
   if (!fn) throw UsageError("p2p_allreduce: unsupported dtype combination");
-  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, s));
+  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   ls.done();
 }
 

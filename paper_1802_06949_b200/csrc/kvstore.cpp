@@ -98,6 +98,7 @@ KvStore::~KvStore() {
   for (KeyState& k : keys_)
     if (k.mom) cudaFree(k.mom);
   for (void* p : allocations_) cudaFree(p);
+  nvls_free(nvls_);
 }
 
 void KvStore::check_key(int key, bool must_be_initialized) const {
@@ -222,8 +223,15 @@ void KvStore::build_buckets() {
   uint64_t total = 0;
   for (Bucket& b : bs) total += b.count;
   engine_.bind_device();
-  char* arena = static_cast<char*>(device_alloc_zeroed(total * es));
-  allocations_.push_back(arena);
+  char* arena = nullptr;
+  if (p2p_active_ && cfg_.p2p == 2 && transport_.nvls_capable()) {
+    // NVLink SHARP: the arena is bound to a multicast object on every rank
+    nvls_ = transport_.alloc_nvls(total * es);
+    arena = static_cast<char*>(nvls_.uc);
+  } else {
+    arena = static_cast<char*>(device_alloc_zeroed(total * es));
+    allocations_.push_back(arena);
+  }
   uint64_t off = 0;
   for (size_t i = 0; i < bs.size(); ++i) {
     Bucket& b = bs[i];
@@ -238,7 +246,14 @@ void KvStore::build_buckets() {
       b.lane = world_lane_;
     }
   }
-  if (p2p_active_) {
+  if (p2p_active_ && nvls_.mc) {
+    for (Bucket& b : bs) {
+      const uint64_t boff = static_cast<uint64_t>(static_cast<char*>(b.base) - arena);
+      b.mc = static_cast<char*>(nvls_.mc) + boff;
+      b.peer_bufs.assign(static_cast<size_t>(transport_.num_ranks()), nullptr);
+      b.peer_bufs[static_cast<size_t>(rank_)] = b.base;
+    }
+  } else if (p2p_active_) {
     // setup-phase collective: every rank maps every peer's arena (CUDA IPC)
     const std::vector<void*> peers = transport_.share_buffer(arena);
     for (Bucket& b : bs) {
@@ -373,7 +388,8 @@ Dispatch KvStore::depcha_dispatch() const {
 void KvStore::collective_body(const Bucket& B, int b, cudaStream_t s, const Transport::P2PUpdate* upd) {
   const int bid = cfg_.bucket_bytes ? b : -1;
   if (p2p_active_) {
-    transport_.allreduce_p2p(B.comm, rank_, B.peer_bufs.data(), B.count, comm_dt_, B.keys[0], s, bid, upd);
+    transport_.allreduce_p2p(B.comm, rank_, B.peer_bufs.data(), B.count, comm_dt_, B.keys[0], s, bid, upd,
+                             B.mc);
   } else {
     transport_.allreduce_sum(B.comm, rank_, B.base, B.count, comm_dt_, B.keys[0], s, bid);
   }
@@ -478,8 +494,11 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
         DeviceTable* ptab = B.p2p_tab.get();  // all its uploads on B.lane
         for (const Tag& t : out_tags) muts.push_back(t);
+        // this op updates every key of the bucket, so nothing reads the
+        // bucket afterwards: keep only the own shard of the sum locally
+        const bool whole = B.pulled == 0 && idxs.size() == B.keys.size();
         engine_.push_stream(
-            [self, bi, es, ptab, out_dt, opt](cudaStream_t s) {
+            [self, bi, es, ptab, out_dt, opt, whole](cudaStream_t s) {
               Transport::P2PUpdate u;
               u.tab = ptab->resident(es, s);
               u.n_entries = static_cast<int>(es.size());
@@ -487,6 +506,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
               u.lr = opt.lr;
               u.rescale = opt.rescale;
               u.momentum = opt.momentum;
+              u.shard_only = whole;
               self->collective_body(self->buckets_[bi], bi, s, &u);
             },
             {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());

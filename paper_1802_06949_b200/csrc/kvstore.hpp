@@ -117,6 +117,7 @@ class KvStore {
     Tag tag;  // engine tag of the whole comm buffer
     std::shared_ptr<DeviceTable> pack_tab, upd_tab, unpack_tab, p2p_tab;  // resident kernel tables
     std::vector<void*> peer_bufs;  // p2p: this bucket on every rank (IPC-mapped)
+    void* mc = nullptr;            // nvls: this bucket's multicast VA
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -154,6 +155,7 @@ class KvStore {
   int initialized_count_ = 0;
   bool built_ = false;
   bool p2p_active_ = false;
+  NvlsBuffer nvls_;  // p2p == 2: the multicast-bound comm arena
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call
   uint32_t stamp_ = 0;
   uint32_t next_stamp() {

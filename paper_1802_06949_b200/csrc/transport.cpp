@@ -125,14 +125,20 @@ std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int n
       ok = ok && can;
     }
     // every rank must agree, or the shared setup below would not match
-    const int32_t mine = ok ? 1 : 0;
+    const int32_t mine = (ok ? 1 : 0) | (nvls_device_supported(device) ? 2 : 0);
     t->ledger_->post_rank_blob(kLedgerRankBlobSlots - 1, rank, &mine, sizeof(mine));
+    bool nvls = true;
     for (int r = 0; r < nranks; ++r) {
       int32_t v = 0;
       t->ledger_->read_rank_blob(kLedgerRankBlobSlots - 1, r, &v, sizeof(v));
-      ok = ok && v;
+      ok = ok && (v & 1);
+      nvls = nvls && (v & 2);
     }
     t->p2p_ok_ = ok;
+    const char* pe = std::getenv("CSB_P2P_PUSH");  // must match on every rank (same environment)
+    t->push_ = !(pe && std::string(pe) == "0");
+    t->nvls_ok_ = ok && nvls;
+    t->name_ = name;
     if (ok) t->setup_flags();
   }
   return t;
@@ -164,6 +170,21 @@ std::vector<void*> Transport::share_buffer(void* base) {
   return ptrs;
 }
 
+NvlsBuffer Transport::alloc_nvls(size_t bytes) {
+  if (!nvls_capable()) throw UsageError("Transport: NVLS multicast unavailable on these devices");
+  int slot;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (share_slots_ + 2 > kLedgerRankBlobSlots - 1) throw ConfigError("Transport: too many shared buffers");
+    slot = share_slots_;
+    share_slots_ += 2;
+  }
+  std::string tag = name_;
+  for (char& c : tag)
+    if (c == '/') c = '_';
+  return nvls_alloc(*ledger_, rank_, num_ranks(), device_, bytes, tag, slot);
+}
+
 void Transport::setup_flags() {
   void* f = nullptr;
   CSB_CUDA(cudaSetDevice(device_));
@@ -174,8 +195,32 @@ void Transport::setup_flags() {
   flags_.push_back(share_buffer(f));
 }
 
+// Called at the same matched op on every rank (the ledger matched the bucket
+// signature first), so the growth and its IPC exchange are collective.  Old
+// areas stay mapped until the transport closes: a peer may still hold them.
+void Transport::ensure_recv(int comm, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (recv_bytes_.size() <= static_cast<size_t>(comm)) {
+      recv_bytes_.resize(static_cast<size_t>(comm) + 1, 0);
+      recv_.resize(static_cast<size_t>(comm) + 1);
+    }
+    if (recv_bytes_[static_cast<size_t>(comm)] >= bytes) return;
+  }
+  const size_t grown = (bytes + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+  CSB_CUDA(cudaSetDevice(device_));
+  void* r = nullptr;
+  CSB_CUDA(cudaMalloc(&r, grown));
+  std::vector<void*> peers = share_buffer(r);
+  std::lock_guard<std::mutex> lock(mu_);
+  own_recv_.push_back(r);
+  recv_[static_cast<size_t>(comm)] = std::move(peers);
+  recv_bytes_[static_cast<size_t>(comm)] = grown;
+}
+
 void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
-                              int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd) {
+                              int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
+                              void* mc) {
   if (!p2p_capable()) throw UsageError("Transport: peer-memory path unavailable");
   if (count == 0) throw UsageError("allreduce_sum: empty buffer");
   CallSig sig;
@@ -188,6 +233,8 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     t = ledger_->arrive(comm, rank, sig, trace_key, bucket);
   }
   if (t.last) ledger_->finish(t);
+  const bool push = push_ && !mc;
+  if (push) ensure_recv(comm, p2p_recv_bytes(count, dtype, num_ranks()));
   P2PArgs a;
   {
     std::lock_guard<std::mutex> lock(mu_);
@@ -195,8 +242,10 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     for (int r = 0; r < num_ranks(); ++r) {
       a.bufs[r] = peer_bufs[r];
       a.flags[r] = static_cast<uint32_t*>(flags_[static_cast<size_t>(comm)][static_cast<size_t>(r)]);
+      if (push) a.recv[r] = recv_[static_cast<size_t>(comm)][static_cast<size_t>(r)];
     }
   }
+  a.mc = mc;
   a.nranks = num_ranks();
   a.rank = rank;
   a.count = count;
@@ -210,6 +259,7 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     a.lr = upd->lr;
     a.rescale = upd->rescale;
     a.momentum = upd->momentum;
+    a.shard_only = upd->shard_only && !mc;
   }
   device_latency(stream);
   p2p_allreduce(a, stream);
@@ -222,6 +272,7 @@ Transport::~Transport() {
     cudaSetDevice(device_);
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (void* p : own_flags_) cudaFree(p);
+    for (void* p : own_recv_) cudaFree(p);
     for (ncclComm_t c : comms_) {
       if (!c) continue;
       if (aborted) ncclCommAbort(c);

@@ -30,6 +30,7 @@
 
 #include "kernels.hpp"
 #include "ledger.hpp"
+#include "nvls.hpp"
 
 namespace csb {
 
@@ -77,12 +78,18 @@ class Transport {
     int n_entries = 0;
     int wdt = CS_F32;
     double lr = 0, rescale = 0, momentum = 0;
+    bool shard_only = false;  // the bucket keeps only this rank's shard (update reads owners)
   };
   // Allreduce of one bucket through peer memory, matched by the ledger like
   // allreduce_sum; with `upd`, fused with the SGD / momentum update of the
   // keys in the bucket (kernels.cu p2p_allreduce_kernel).
   void allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
-                     int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd);
+                     int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
+                     void* mc = nullptr);
+  // NVLink SHARP: every rank's device supports multicast objects.
+  bool nvls_capable() const { return p2p_capable() && nvls_ok_; }
+  // Setup-phase collective: a multicast-bound allocation (nvls.hpp).
+  NvlsBuffer alloc_nvls(size_t bytes);
 
  private:
   Transport() = default;
@@ -103,10 +110,18 @@ class Transport {
   // peer-memory path
   void setup_flags();  // one flag region per communicator, shared
   bool p2p_ok_ = false;
+  bool nvls_ok_ = false;
+  std::string name_;
   int share_slots_ = 0;
   std::vector<void*> ipc_opened_;
   std::vector<void*> own_flags_;
   std::vector<std::vector<void*>> flags_;  // comm -> every rank's flag region
+  // push mode: comm -> every rank's receive area (grown collectively, never shrunk)
+  void ensure_recv(int comm, size_t bytes);
+  bool push_ = true;
+  std::vector<std::vector<void*>> recv_;
+  std::vector<size_t> recv_bytes_;
+  std::vector<void*> own_recv_;
 };
 
 }  // namespace csb

@@ -62,7 +62,8 @@ def main():
         eng.close()
     elif case.split("_")[0] in ("funnel", "depcha", "concom"):
         mode = case.split("_")[0]
-        p2p = case.endswith("_p2p")
+        split = case.endswith("_p2psplit")  # one pull_update per key: buckets not whole
+        p2p = case.endswith("_p2p") or split
         gold = np.load(HERE / "golden" / "train_steps.npz")
         sizes = [int(x) for x in gold["sizes"]]
         K, lr, rescale = len(sizes), float(gold["lr"]), 1.0 / (64 * world)
@@ -85,7 +86,11 @@ def main():
                 sp, dp, n = src[k].data_ptr(), gs[k].value.data_ptr(), sizes[k]
                 eng.push_stream(lambda st, sp=sp, dp=dp, n=n: api.synth_backward(sp, dp, n, api.F64, 0, 0, st),
                                 [], [gs[k].tag], api.COMPUTE, k)
-            if case_mode == "depcha":
+            if case_mode == "depcha" and split:
+                store.push(list(range(K)), gs)
+                for k in range(K):
+                    store.pull_update(k, ws[k], lr, rescale)
+            elif case_mode == "depcha":
                 store.push(list(range(K)), gs)
                 store.pull_update(list(range(K)), ws, lr, rescale)
             else:
@@ -101,6 +106,54 @@ def main():
                 if case_mode == "concom" and since:
                     store.barrier()
             eng.wait_all()
+        np.savez(outdir / f"{case}_r{rank}.npz", *[w.value.cpu().numpy() for w in ws])
+        store.close()
+        eng.close()
+    elif case == "p2p_api":
+        # cs_allreduce_p2p directly: reduce only, fused update keeping the
+        # whole sum, fused update keeping only the own shard (shard_only)
+        n = 4 << 20  # 16 MiB fp32: its own allocator segment, so the IPC base is the tensor
+        eng = Engine(1, rank, None, local)
+        s = eng.lane_stream(0)
+        g = torch.from_numpy(O.random_uniform(n, 1000 + rank).astype(np.float32)).to(dev)
+        w0 = torch.from_numpy(O.random_uniform(n, O.mix_seed(7, 0)).astype(np.float32)).to(dev)
+        buf = torch.empty(n, dtype=torch.float32, device=dev)
+        peers = tr.share_buffer(buf.data_ptr())
+        res = {}
+        buf.copy_(g)
+        torch.cuda.synchronize(dev)
+        tr.allreduce_p2p(0, rank, peers, n, api.F32, 0, None, s)
+        torch.cuda.synchronize(dev)
+        res["sum"] = buf.cpu().numpy()
+        for so in (0, 1):
+            buf.copy_(g)
+            w = w0.clone()
+            m = torch.zeros(n, dtype=torch.float32, device=dev)
+            torch.cuda.synchronize(dev)
+            ents = [(w.data_ptr(), buf.data_ptr(), m.data_ptr(), n)]
+            tr.allreduce_p2p(0, rank, peers, n, api.F32, 1, (ents, api.F32, 0.1, 1.0 / 64, 0.9, so), s)
+            torch.cuda.synchronize(dev)
+            res[f"w{so}"], res[f"m{so}"], res[f"buf{so}"] = w.cpu().numpy(), m.cpu().numpy(), buf.cpu().numpy()
+        np.savez(outdir / f"{case}_r{rank}.npz", **res)
+        eng.close()
+    elif case == "nvls":
+        # fp32 DepCha over NVSwitch multicast (in-switch reduction): the test
+        # compares with the fp64 oracle of the fp32-rounded inputs
+        sizes = [1, 7, 64, 300, 4097, 70000]
+        K = len(sizes)
+        eng = Engine(4, rank, sink, local)
+        store = KvStore(eng, tr, rank, KvConfig("depcha", 1, K, bucket_bytes=64 * 1024, p2p=2))
+        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)  # noqa: E731
+        ws = [Slot(f32(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n)), eng.new_variable())
+              for k, n in enumerate(sizes)]
+        gs = [Slot(f32(O.random_uniform(n, 1000 + rank * K + k)), eng.new_variable()) for k, n in enumerate(sizes)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        store.push(list(range(K)), gs)
+        store.pull_update(list(range(K)), ws, 0.1, 1.0 / 64, 0.9)
+        eng.wait_all()
+        out["nvls_active"] = bool(tr.p2p_capable())
         np.savez(outdir / f"{case}_r{rank}.npz", *[w.value.cpu().numpy() for w in ws])
         store.close()
         eng.close()

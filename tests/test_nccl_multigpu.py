@@ -105,6 +105,76 @@ def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path):
             assert outs[r]["trace"] == outs[0]["trace"]
 
 
+def test_p2p_split_pulls_bit_exact(two_gpus, tmp_path):
+    """Same, but one pull_update per key: the first pull of a bucket fuses only
+    its own key's update, so the kernel keeps the whole sum in every bucket
+    (shard_only off) and the later pulls read it."""
+    gold = np.load(HERE / "golden" / "train_steps.npz")
+    K = len(gold["sizes"])
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("depcha_p2psplit", R, d)
+        for r in range(R):
+            w = np.load(d / f"depcha_p2psplit_r{r}.npz")
+            for k in range(K):
+                np.testing.assert_array_equal(w[f"arr_{k}"], gold[f"depcha_R{R}_r{r}_k{k}"])
+
+
+def test_p2p_c_abi_reduce_and_shard_only(two_gpus, tmp_path):
+    """cs_allreduce_p2p on a 16 MiB fp32 bucket: the reduce-only sum is the
+    fp32 rank-order sum bit for bit; the fused update gives identical weights
+    and momentum with shard_only 0 and 1; shard_only 0 leaves the whole sum in
+    the bucket, shard_only 1 exactly the own shard; weights and momentum match
+    the f32 oracle update bit for bit."""
+    n = 4 << 20
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("p2p_api", R, d)
+        gs = [O.random_uniform(n, 1000 + r).astype(np.float32) for r in range(R)]
+        exp = gs[0].copy()
+        for x in gs[1:]:
+            exp = exp + x  # float32 IEEE round-to-nearest, rank order
+        w0 = O.random_uniform(n, O.mix_seed(7, 0)).astype(np.float32)
+        w_exp, m_exp = O.sgd_update(w0, exp, 0.1, 1.0 / 64, 0.9, np.zeros(n, np.float32), kind="f32")
+        groups = n // 8
+        outs = [np.load(d / f"p2p_api_r{r}.npz") for r in range(R)]
+        for r, o in enumerate(outs):
+            np.testing.assert_array_equal(o["sum"], exp)
+            np.testing.assert_array_equal(o["buf0"], exp)
+            np.testing.assert_array_equal(o["w0"], o["w1"])
+            np.testing.assert_array_equal(o["m0"], o["m1"])
+            a, b = 8 * (groups * r // R), 8 * (groups * (r + 1) // R)
+            np.testing.assert_array_equal(o["buf1"][a:b], exp[a:b])
+            np.testing.assert_array_equal(o["m0"], m_exp)
+            np.testing.assert_array_equal(o["w0"], w_exp)
+            np.testing.assert_array_equal(o["w0"], outs[0]["w0"])
+
+
+def test_nvls_fused_allreduce_update_within_tolerance(two_gpus, tmp_path):
+    """fp32 DepCha through the NVSwitch multicast path (multimem.ld_reduce /
+    multimem.st) fused with the momentum update: within the north-star fp32
+    tolerance of the fp64 oracle, and identical on every rank."""
+    sizes = [1, 7, 64, 300, 4097, 70000]
+    K = len(sizes)
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("nvls", R, d)
+        ws = [np.load(d / f"nvls_r{r}.npz") for r in range(R)]
+        for k, n in enumerate(sizes):
+            g = [O.random_uniform(n, 1000 + r * K + k).astype(np.float32).astype(np.float64) for r in range(R)]
+            s = O.rank_order_sum(g, "f64")
+            w0 = O.random_uniform(n, O.mix_seed(7, k)).astype(np.float32).astype(np.float64)
+            exp, _ = O.sgd_update(w0, s, 0.1, 1.0 / 64, 0.9, np.zeros(n))
+            scale = np.abs(w0) + 0.1 / 64 * np.sum([np.abs(x) for x in g], axis=0)
+            for r in range(R):
+                got = ws[r][f"arr_{k}"].astype(np.float64)
+                assert np.all(np.abs(got - exp) <= 1e-6 * scale + 1e-7), (R, k)
+                np.testing.assert_array_equal(ws[r][f"arr_{k}"], ws[0][f"arr_{k}"])
+
+
 def test_cross_process_mismatch_raises_before_nccl(two_gpus, tmp_path):
     outs = run_case("mismatch", 2, tmp_path)
     assert [o["error"] for o in outs] == ["MismatchError", "MismatchError"]

@@ -20,6 +20,11 @@ import torch.distributed as dist  # noqa: E402
 from paper_1802_06949_b200 import api  # noqa: E402
 
 
+def busbw_of(n, world, us):
+    """nccl-tests bus bandwidth of an allreduce of n fp32 elements, GB/s."""
+    return round(4 * n * 2 * (world - 1) / world / (us * 1e3), 1)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--mb", type=float, nargs="+", default=[1, 4, 25, 100])
@@ -65,10 +70,20 @@ def main():
         r["p2p_us"] = timed(lambda: tr.allreduce_p2p(0, rank, peers, n, api.F32, 0, None, sh))
         r["p2p_fused_sgd_us"] = timed(lambda: tr.allreduce_p2p(0, rank, peers, n, api.F32, 0,
                                                                (ent, api.F32, 0.1, 1e-3, 0.9), sh))
+        r["p2p_fused_sgd_shard_us"] = timed(lambda: tr.allreduce_p2p(0, rank, peers, n, api.F32, 0,
+                                                                     (ent, api.F32, 0.1, 1e-3, 0.9, 1), sh))
         r["sgd_only_us"] = timed(lambda: api.sgd_update(ent, api.F32, api.F32, 0.1, 1e-3, 0.9, sh))
-        busbw = lambda us: round(4 * n * 2 * (world - 1) / world / (us * 1e3), 1)  # GB/s
-        r["nccl_busbw"] = busbw(r["nccl_us"])
-        r["p2p_busbw"] = busbw(r["p2p_us"])
+        if tr.nvls_capable():
+            uc, mc = tr.alloc_nvls(4 * n)
+            api.pack([(buf.data_ptr(), uc, n)], api.F32, api.F32, sh)
+            torch.cuda.synchronize()
+            entv = [(w.data_ptr(), uc, m.data_ptr(), n)]
+            r["nvls_us"] = timed(lambda: tr.allreduce_nvls(0, rank, uc, mc, n, api.F32, 0, None, sh))
+            r["nvls_fused_sgd_us"] = timed(lambda: tr.allreduce_nvls(0, rank, uc, mc, n, api.F32, 0,
+                                                                     (entv, api.F32, 0.1, 1e-3, 0.9), sh))
+            r["nvls_busbw"] = busbw_of(n, world, r["nvls_us"])
+        r["nccl_busbw"] = busbw_of(n, world, r["nccl_us"])
+        r["p2p_busbw"] = busbw_of(n, world, r["p2p_us"])
         res[f"{mb}MB"] = r
     if rank == 0:
         print(json.dumps({"world": world, "results": res}))
