@@ -44,7 +44,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "aggregated gradient GB/s/GPU & exposed comm ms/iter at 1/2/4/8 B200"
 CONFIGS = {
     # name: (keyset, mode, outstanding, dtype, bucket_mb, backward calibration or fixed ms)
-    "resnet50": ("resnet50", "depcha", 1, "fp32", 50, "resnet50_b64.json"),
+    "resnet50": ("resnet50", "depcha", 1, "fp32", 100, "resnet50_b64.json"),
     "alexnet": ("alexnet", "concom", 4, "fp32", 25, "alexnet_b64_amp.json"),
     "resnet152": ("resnet152", "depcha", 1, "bf16", 25, "resnet152_b64_amp.json"),
     "inception_v3": ("inception_v3", "depcha", 1, "bf16", 25, 30.0),
@@ -83,8 +83,9 @@ def parse():
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
-    p.add_argument("--comm", default="nccl", choices=["nccl", "p2p", "nvls"],
-                   help="collective engine for N>1: NCCL, or the fused NVLink peer-memory kernel")
+    p.add_argument("--comm", default=None, choices=["nccl", "p2p", "nvls"],
+                   help="collective engine for N>1: the fused NVLink peer-memory kernel (default; "
+                        "NCCL for ConCom, whose extra communicators run concurrently), NCCL, or NVLS")
     return p.parse_args()
 
 
@@ -236,6 +237,8 @@ def main():
               "l2": "inputs larger than L2 (no flush)"}
     if args.impl == "reference":
         return reference_main(args, args.config, keys, mode, outstanding, config)
+    if args.comm is None:
+        args.comm = "nccl" if mode == "concom" else "p2p"
 
     import torch
     import torch.distributed as dist
@@ -341,18 +344,32 @@ def main():
         api.profile_enable(True)
         model.run(max(3, min(args.steps, 10)), COMM)
         api.profile_enable(False)
+        n_prof = max(3, min(args.steps, 10))
         kstats = {k: api.profile_collect(k) for k in ("pack", "sum", "sgd")}
         dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
         ks = kstats[dom]
         pk = peaks()
-        peak = pk.get("hbm_gbs", 6650.0)
-        achieved = ks["bytes"] / (ks["total_ms"] * 1e6) if ks["total_ms"] > 0 else 0.0
-        line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+        if world > 1 and args.comm in ("p2p", "nvls") and dom == "sum":
+            # the fused allreduce+update kernel is NVLink-bound: algorithmic
+            # bytes crossing the link per GPU per direction, per step
+            # (peer loads: 2(N-1)/N x bucket bytes; NVLS: 1 x bucket bytes)
+            link_step = gbytes * (2.0 * (world - 1) / world if args.comm == "p2p" else 1.0)
+            bytes_launch = link_step * n_prof / max(1, ks["launches"])
+            bound, peak = "nvlink", pk.get("nvlink_gbs_per_dir", 770.0)
+            peak_source = ("MEASURED_PEAKS.json nvlink_gbs_per_dir" if "nvlink_gbs_per_dir" in pk else
+                           "B200_PROFILING.md measured peer copy, 770 GB/s per direction")
+        else:
+            bytes_launch = ks["bytes"] / max(1, ks["launches"])
+            bound, peak = "hbm", pk.get("hbm_gbs", 6650.0)
+            peak_source = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"
+        avg_s = ks["total_ms"] / max(1, ks["launches"]) / 1e3
+        achieved = bytes_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+        line["roofline"] = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                             "launches": ks["launches"],
                             "avg_launch_us": round(1000 * ks["total_ms"] / max(1, ks["launches"]), 2),
-                            "bytes_per_launch": round(ks["bytes"] / max(1, ks["launches"])),
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback",
+                            "bytes_per_launch": round(bytes_launch),
+                            "peak_source": peak_source,
                             "kernels": {k: {"launches": v["launches"],
                                             "ms_per_step": round(v["total_ms"] / max(3, min(args.steps, 10)), 4),
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}

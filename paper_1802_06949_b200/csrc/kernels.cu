@@ -634,27 +634,46 @@ __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a,
 // within tolerance, not bit-exact (the IPC path above is bit-exact).
 template <int CDT>
 __device__ __forceinline__ void nvls_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
-  if (threadIdx.x >= kP2PLinkThreads) return;
-  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+  // 16-byte vectors; the multicast ops have long latency, so every thread
+  // keeps U reductions in flight and all 512 threads take part (no peer
+  // load queues to protect here)
+  constexpr uint64_t kVPG = (CDT == CS_F32) ? 2 : 1;  // vectors per group
+  constexpr int U = 4;
+  const uint64_t va = a * kVPG, vb = b * kVPG;
+  auto ld = [&](uint64_t v, uint32_t (&r)[4]) {
     if constexpr (CDT == CS_F32) {
-      float* base = static_cast<float*>(p.mc) + q * kVec;
-      float v[8];
+      const float* ptr = static_cast<const float*>(p.mc) + v * 4;
       asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(base) : "memory");
-      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "l"(base + 4) : "memory");
-      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
-                   ::"l"(base), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
-      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
-                   ::"l"(base + 4), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(ptr) : "memory");
     } else {
-      __nv_bfloat16* base = static_cast<__nv_bfloat16*>(p.mc) + q * kVec;
-      uint32_t v[4];
+      const __nv_bfloat16* ptr = static_cast<const __nv_bfloat16*>(p.mc) + v * 8;
       asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(base) : "memory");
-      asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};"
-                   ::"l"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(ptr) : "memory");
     }
+  };
+  auto st = [&](uint64_t v, const uint32_t (&r)[4]) {
+    if constexpr (CDT == CS_F32) {
+      float* ptr = static_cast<float*>(p.mc) + v * 4;
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                   ::"l"(ptr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+    } else {
+      __nv_bfloat16* ptr = static_cast<__nv_bfloat16*>(p.mc) + v * 8;
+      asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};"
+                   ::"l"(ptr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+    }
+  };
+  uint64_t v = va + threadIdx.x;
+  for (; v + (U - 1) * kP2PThreads < vb; v += U * kP2PThreads) {
+    uint32_t r[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ld(v + u * kP2PThreads, r[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st(v + u * kP2PThreads, r[u]);
+  }
+  for (; v < vb; v += kP2PThreads) {
+    uint32_t r[4];
+    ld(v, r);
+    st(v, r);
   }
 }
 

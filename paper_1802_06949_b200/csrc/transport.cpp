@@ -135,8 +135,11 @@ std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int n
       nvls = nvls && (v & 2);
     }
     t->p2p_ok_ = ok;
-    const char* pe = std::getenv("CSB_P2P_PUSH");  // must match on every rank (same environment)
-    t->push_ = !(pe && std::string(pe) == "0");
+    // push mode (writes-only NVLink traffic) measured slower than peer loads
+    // on B200 (tools/nvlink_probe.cu); opt in with CSB_P2P_PUSH=1,
+    // identically on every rank
+    const char* pe = std::getenv("CSB_P2P_PUSH");
+    t->push_ = pe && std::string(pe) == "1";
     t->nvls_ok_ = ok && nvls;
     t->name_ = name;
     if (ok) t->setup_flags();
