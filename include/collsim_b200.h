@@ -128,6 +128,17 @@ int cs_engine_push_stream(cs_engine_t e, cs_stream_fn fn, void* arg, const uint6
                           int lane, int dispatch, uint64_t* op_id);
 int cs_engine_wait_for(cs_engine_t e, uint64_t tag);
 int cs_engine_wait_all(cs_engine_t e);
+/* Interop with a framework's own CUDA stream (no reference counterpart: the
+ * reference's producers are engine ops, trainer.cpp:36-72).
+ * import_event: stream op on `lane` that waits on `cuda_event` (a cudaEvent_t
+ * the caller recorded after producing the tensors) and mutates `mutates`; the
+ * event may be re-recorded once the op is dispatched (inline, normally inside
+ * this call).  stream_wait: waits on the host until every op pushed so far on
+ * `tags` is dispatched, then makes `stream` wait on their last write and the
+ * reads since (the external stream may then read or overwrite the tensors). */
+int cs_engine_import_event(cs_engine_t e, void* cuda_event, const uint64_t* mutates, int n_mutates,
+                           int key, int lane, uint64_t* op_id);
+int cs_engine_stream_wait(cs_engine_t e, const uint64_t* tags, int n_tags, cs_stream_t stream);
 int cs_engine_shutdown(cs_engine_t e);
 int cs_engine_new_lane(cs_engine_t e, int priority, int* lane);
 int cs_engine_lane_stream(cs_engine_t e, int lane, cs_stream_t* out);
@@ -229,6 +240,8 @@ int cs_kv_barrier(cs_kvstore_t kv);
 int cs_kv_outstanding_in_flight(cs_kvstore_t kv, int* out);
 /* synchronizes the key's comm buffer and copies it to host memory (comm dtype) */
 int cs_kv_comm_buf(cs_kvstore_t kv, int key, void* host_out, uint64_t* numel, int* dtype);
+/* key -> (fusion bucket, element offset); builds the buckets once every key is
+ * initialized (with the peer-memory path a setup collective: all ranks call it) */
 int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems);
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
 int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);

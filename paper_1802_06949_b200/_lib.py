@@ -82,6 +82,8 @@ SIGNATURES = {
     "cs_engine_push_stream": [_P, STREAM_FN, _P, _PU64, _I, _PU64, _I, _I, _I, _I, _I, _PU64],
     "cs_engine_wait_for": [_P, _U64],
     "cs_engine_wait_all": [_P],
+    "cs_engine_import_event": [_P, _P, _PU64, _I, _I, _I, _PU64],
+    "cs_engine_stream_wait": [_P, _PU64, _I, _P],
     "cs_engine_shutdown": [_P],
     "cs_engine_new_lane": [_P, _I, _PI],
     "cs_engine_lane_stream": [_P, _I, C.POINTER(_P)],

@@ -203,6 +203,19 @@ class Engine:
     def wait_for(self, tag: int) -> None:
         check(lib.cs_engine_wait_for(self.h, tag))
 
+    def import_event(self, cuda_event: int, mutates: Iterable[int], key: int = -1, lane: int = 0) -> int:
+        """The writes recorded by `cuda_event` (on an external stream) become
+        the latest writes of `mutates`."""
+        m, nm = _u64_array(list(mutates))
+        op = C.c_uint64()
+        check(lib.cs_engine_import_event(self.h, cuda_event, m, nm, key, lane, C.byref(op)))
+        return op.value
+
+    def stream_wait(self, tags: Iterable[int], stream: int) -> None:
+        """Make an external stream wait for every op pushed so far on `tags`."""
+        t, nt = _u64_array(list(tags))
+        check(lib.cs_engine_stream_wait(self.h, t, nt, stream))
+
     def wait_all(self) -> None:
         check(lib.cs_engine_wait_all(self.h))
 

@@ -229,6 +229,21 @@ int cs_engine_wait_for(cs_engine_t e, uint64_t tag) {
     e->e->wait_for(e->e->tag_of(tag));
   });
 }
+int cs_engine_import_event(cs_engine_t e, void* cuda_event, const uint64_t* mutates, int n_mutates,
+                           int key, int lane, uint64_t* op_id) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    OpId id = e->e->import_event(static_cast<cudaEvent_t>(cuda_event), tags_of(*e->e, mutates, n_mutates),
+                                 key, lane);
+    if (op_id) *op_id = id;
+  });
+}
+int cs_engine_stream_wait(cs_engine_t e, const uint64_t* tags, int n_tags, cs_stream_t stream) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    e->e->stream_wait(tags_of(*e->e, tags, n_tags), reinterpret_cast<cudaStream_t>(stream));
+  });
+}
 int cs_engine_wait_all(cs_engine_t e) {
   return guard([&] {
     CHECK_HANDLE(e);

@@ -488,6 +488,30 @@ void Engine::wait_for(const Tag& tag) {
   }
 }
 
+OpId Engine::import_event(cudaEvent_t ev, const std::vector<Tag>& mutates, int key, int lane) {
+  if (!ev) throw UsageError("Engine::import_event: null event");
+  return push_stream([ev](cudaStream_t s) { CSB_CUDA(cudaStreamWaitEvent(s, ev, 0)); }, {}, mutates,
+                     OpKind::Other, key, lane, Dispatch::Inline);
+}
+
+void Engine::stream_wait(const std::vector<Tag>& tags, cudaStream_t stream) {
+  std::vector<EventRef> evs;
+  {
+    std::unique_lock<std::mutex> lock(mu_);
+    for (const Tag& tag : tags) {
+      VarRecord& var = var_for(tag);
+      control_cv_.wait(lock, [&var] { return var.queue.empty(); });
+      if (var.last_write) evs.push_back(var.last_write);
+      for (const EventRef& r : var.readers) evs.push_back(r);
+    }
+  }
+  std::sort(evs.begin(), evs.end());
+  evs.erase(std::unique(evs.begin(), evs.end()), evs.end());
+  if (evs.empty()) return;
+  bind_device();
+  for (const EventRef& e : evs) CSB_CUDA(cudaStreamWaitEvent(stream, e->ev, 0));
+}
+
 void Engine::wait_all() {
   {
     std::unique_lock<std::mutex> lock(mu_);

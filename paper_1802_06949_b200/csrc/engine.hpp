@@ -86,6 +86,15 @@ class Engine {
 
   void wait_for(const Tag& tag);
   void wait_all();
+
+  // Interop with an external CUDA stream (a framework's compute stream).
+  // import_event: a stream op on `lane` that waits on `ev` and mutates
+  // `mutates` -- the external producer's writes (recorded by `ev`) become the
+  // tags' latest writes.  stream_wait: blocks the host until every op pushed
+  // so far on `tags` is dispatched, then makes `stream` wait on their last
+  // write and the reads since, so the external stream may read or write them.
+  OpId import_event(cudaEvent_t ev, const std::vector<Tag>& mutates, int key = -1, int lane = 0);
+  void stream_wait(const std::vector<Tag>& tags, cudaStream_t stream);
   void shutdown();
 
   // Lane 0 exists from construction (the compute lane).  priority follows

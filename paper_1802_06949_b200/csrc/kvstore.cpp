@@ -112,10 +112,10 @@ uint64_t KvStore::key_numel(int key) const {
   return keys_[static_cast<size_t>(key)].numel;
 }
 
-void KvStore::key_map(int key, int* bucket, uint64_t* offset) const {
+void KvStore::key_map(int key, int* bucket, uint64_t* offset) {
   check_key(key, true);
   const KeyState& k = keys_[static_cast<size_t>(key)];
-  if (k.bucket < 0) throw UsageError("KvStore: fusion buckets are built at the first push");
+  if (k.bucket < 0) build_buckets();  // UsageError until every key is initialized
   *bucket = k.bucket;
   *offset = k.offset;
 }

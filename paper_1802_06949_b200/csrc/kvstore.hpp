@@ -89,7 +89,9 @@ class KvStore {
   void comm_buf(int key, void* host_out);
   int comm_dtype() const { return comm_dt_; }
   uint64_t key_numel(int key) const;
-  void key_map(int key, int* bucket, uint64_t* offset) const;
+  // Builds the fusion buckets first when every key is initialized (a
+  // setup-phase collective with the peer-memory path: call it on every rank).
+  void key_map(int key, int* bucket, uint64_t* offset);
   int num_buckets() const { return static_cast<int>(buckets_.size()); }
   int bucket_lane(int b) const;
   // Keys of every comm bucket, buckets in issue order (builds the map).

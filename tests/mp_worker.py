@@ -136,6 +136,29 @@ def main():
             res[f"w{so}"], res[f"m{so}"], res[f"buf{so}"] = w.cpu().numpy(), m.cpu().numpy(), buf.cpu().numpy()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)
         eng.close()
+    elif case == "torch_dp":
+        # real-backward producer over the fused NVLink kernel: save every
+        # rank's per-step gradients and weights; the test replays the oracle
+        from paper_1802_06949_b200.torch_dp import TorchKvStoreDP
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).to(dev)
+        eng = Engine(4, rank, sink, local)
+        dp = TorchKvStoreDP(model, eng, tr, rank, world, lr=0.05, momentum=0.9, bucket_mb=0.05, p2p=1)
+        flat = lambda ts: np.concatenate([t.detach().cpu().numpy().ravel() for t in ts])  # noqa: E731
+        res = {"w0": flat(dp.params), "buckets": np.array(len(dp.groups))}
+        gen = torch.Generator(device=dev).manual_seed(100 + rank)
+        for step in range(3):
+            x = torch.randn(16, 64, device=dev, generator=gen)
+            y = torch.randint(0, 10, (16,), device=dev, generator=gen)
+            dp.zero_grad()
+            torch.nn.functional.cross_entropy(model(x), y).backward()
+            dp.step()
+            torch.cuda.synchronize(dev)
+            res[f"g{step}"] = flat([p.grad for p in dp.params])
+            res[f"w{step + 1}"] = flat(dp.params)
+        np.savez(outdir / f"{case}_r{rank}.npz", **res)
+        dp.close()
+        eng.close()
     elif case == "nvls":
         # fp32 DepCha over NVSwitch multicast (in-switch reduction): the test
         # compares with the fp64 oracle of the fp32-rounded inputs

@@ -152,6 +152,29 @@ def test_p2p_c_abi_reduce_and_shard_only(two_gpus, tmp_path):
             np.testing.assert_array_equal(o["w0"], outs[0]["w0"])
 
 
+def test_torch_producer_over_nvlink_bit_exact(two_gpus, tmp_path):
+    """PyTorch autograd as the producer (torch_dp.TorchKvStoreDP, 2-3 fusion
+    buckets, fused NVLink kernel): every rank's weights after each step are
+    the f32 oracle update with the rank-order sum of the ranks' gradients."""
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("torch_dp", R, d)
+        outs = [np.load(d / f"torch_dp_r{r}.npz") for r in range(R)]
+        assert int(outs[0]["buckets"]) >= 2
+        w = outs[0]["w0"].astype(np.float32)
+        mom = np.zeros_like(w)
+        for r in range(R):
+            np.testing.assert_array_equal(outs[r]["w0"], w)  # rank 0's weights were broadcast
+        for step in range(3):
+            g = outs[0][f"g{step}"].astype(np.float32)
+            for r in range(1, R):
+                g = g + outs[r][f"g{step}"].astype(np.float32)  # rank order, f32 round-to-nearest
+            w, mom = O.sgd_update(w, g, 0.05, 1.0 / R, 0.9, mom, kind="f32")
+            for r in range(R):
+                np.testing.assert_array_equal(outs[r][f"w{step + 1}"], w, err_msg=f"R={R} rank {r} step {step}")
+
+
 def test_nvls_fused_allreduce_update_within_tolerance(two_gpus, tmp_path):
     """fp32 DepCha through the NVSwitch multicast path (multimem.ld_reduce /
     multimem.st) fused with the momentum update: within the north-star fp32
