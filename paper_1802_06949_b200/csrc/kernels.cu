@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1174,20 +1175,22 @@ struct ChecksumScratch {
 }  // namespace
 
 void checksum(const void* x, uint64_t n, int dt, double* out, cudaStream_t s) {
+  // scratch per (device, stream): checksums on different streams of one
+  // device (rank threads sharing a GPU) must not share the last-block counter
   static std::mutex mu;
-  static std::vector<ChecksumScratch> per_dev;
+  static std::map<std::pair<int, cudaStream_t>, ChecksumScratch> scratch;
   int dev = 0;
   CSB_CUDA(cudaGetDevice(&dev));
   ChecksumScratch sc;
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
-    if (!per_dev[dev].partial) {
-      CSB_CUDA(cudaMalloc(&per_dev[dev].partial, kSumBlocks * sizeof(double)));
-      CSB_CUDA(cudaMalloc(&per_dev[dev].counter, sizeof(unsigned int)));
-      CSB_CUDA(cudaMemset(per_dev[dev].counter, 0, sizeof(unsigned int)));
+    ChecksumScratch& e = scratch[{dev, s}];
+    if (!e.partial) {
+      CSB_CUDA(cudaMalloc(&e.partial, kSumBlocks * sizeof(double)));
+      CSB_CUDA(cudaMalloc(&e.counter, sizeof(unsigned int)));
+      CSB_CUDA(cudaMemset(e.counter, 0, sizeof(unsigned int)));
     }
-    sc = per_dev[dev];
+    sc = e;
   }
   LaunchScope ls(kKernChecksum, static_cast<double>(n) * dtype_size(dt), s);
   switch (dt) {

@@ -41,11 +41,12 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--batch", type=int, default=64)
-    ap.add_argument("--bucket-mb", type=float, default=25.0)
+    ap.add_argument("--bucket-mb", type=float, default=50.0)
     ap.add_argument("--comm", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--momentum", type=float, default=0.9)
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--channels-last", action="store_true")
+    ap.add_argument("--metrics-out", default=None, help="write collsim-metrics-v1 (rank 0)")
     a = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -87,8 +88,10 @@ def main():
 
         def step():
             dp.zero_grad()
-            lossf(model(x), y).backward()
+            loss = lossf(model(x), y)
+            loss.backward()
             dp.step()
+            return loss
     else:
         from torch.nn.parallel import DistributedDataParallel as DDP
         net = DDP(model, device_ids=[local], bucket_cap_mb=a.bucket_mb, gradient_as_bucket_view=True) \
@@ -97,8 +100,10 @@ def main():
 
         def step():
             opt.zero_grad(set_to_none=False)
-            lossf(net(x), y).backward()
+            loss = lossf(net(x), y)
+            loss.backward()
             opt.step()
+            return loss
 
     for _ in range(a.warmup):
         step()
@@ -109,14 +114,26 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(a.steps):
-        step()
+        loss = step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
+    last_loss = loss.detach().float()
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
+        dist.all_reduce(last_loss, op=dist.ReduceOp.SUM)
+        last_loss /= world
+    if a.metrics_out and rank == 0:
+        from paper_1802_06949_b200.metrics import Metrics, write_metrics
+        write_metrics(Metrics(mode="depcha" if a.impl != "ddp" else "ddp", model="torchvision-resnet50",
+                              workers=world, engine_threads=4, outstanding=1, epochs=1,
+                              global_batch=a.batch * world, seed=1000, epoch_times_s=[ms * a.steps / 1e3],
+                              final_train_loss=float(last_loss.item()), test_accuracy=0.0,
+                              max_concurrent_collectives=1, compute_overlap_observed=True,
+                              b200={"impl": a.impl, "comm": a.comm, "steps": a.steps, "ms_per_step": ms,
+                                    "test_accuracy": "n/a (synthetic data)"}), a.metrics_out)
     if rank == 0:
         print(json.dumps({"tool": "train_resnet50", "impl": a.impl, "comm": a.comm if a.impl == "kv" else None,
                           "n_gpus": world, "batch_per_gpu": a.batch, "ms_per_step": round(ms, 3),
