@@ -83,6 +83,9 @@ def parse():
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--grad-views", action="store_true",
+                   help="gradients produced in place in the comm buckets (gradient-as-bucket-view): "
+                        "push copies nothing")
     p.add_argument("--comm", default=None, choices=["nccl", "p2p", "nvls"],
                    help="collective engine for N>1: the fused NVLink peer-memory kernel (default; "
                         "NCCL for ConCom, whose extra communicators run concurrently), NCCL, or NVLS")
@@ -234,7 +237,9 @@ def main():
     config = {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
               "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
               "issue_order": args.issue_order, "momentum": args.momentum, "parallelism": f"dp{world}",
-              "l2": "inputs larger than L2 (no flush)"}
+              "l2": "inputs larger than L2 (no flush)",
+              "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
+              else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"}
     if args.impl == "reference":
         return reference_main(args, args.config, keys, mode, outstanding, config)
     if args.comm is None:
@@ -272,7 +277,7 @@ def main():
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
-                  p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm])
+                  p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views)
     config["collectives"] = ("identity (1 rank)" if world == 1 else
                              {"nccl": "NCCL",
                               "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
@@ -374,6 +379,21 @@ def main():
                                             "ms_per_step": round(v["total_ms"] / max(3, min(args.steps, 10)), 4),
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}
                                         for k, v in kstats.items()}}
+
+        # ---- the same aggregation with gradient-as-bucket-view (no pack copy)
+        if not args.grad_views and bucket_mb > 0:
+            model_v = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main,
+                                     **{**common, "grad_views": True})
+            model_v.init()
+            model_v.run(args.warmup, COMM)
+            barrier()
+            ms_v = max_over_ranks(model_v.run(args.steps, COMM)) / args.steps
+            line["grad_views"] = {"value": round(world * gbytes / (ms_v * 1e6), 3), "unit": "GB/s",
+                                  "ms_per_step": round(ms_v, 4),
+                                  "note": "gradients produced in place in the comm buckets (DDP "
+                                          "gradient_as_bucket_view): push copies nothing; same collective "
+                                          "and fused update"}
+            model_v.close()
 
         # ---- end to end through the C ABI with host buffers
         model_e2e = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_e2e,

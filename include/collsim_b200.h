@@ -243,6 +243,13 @@ int cs_kv_comm_buf(cs_kvstore_t kv, int key, void* host_out, uint64_t* numel, in
 /* key -> (fusion bucket, element offset); builds the buckets once every key is
  * initialized (with the peer-memory path a setup collective: all ranks call it) */
 int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems);
+/* Bucket views (gradient-as-bucket-view): the device address of the key's slot
+ * in its comm bucket (comm dtype).  A gradient written there and pushed with
+ * that address is not copied; the collective rewrites it in place (the whole
+ * sum after a pull, only this rank's shard after a shard_only fused update).
+ * cs_kv_arena: the one allocation holding every fusion bucket (to zero it). */
+int cs_kv_bucket_view(cs_kvstore_t kv, int key, void** ptr);
+int cs_kv_arena(cs_kvstore_t kv, void** base, uint64_t* bytes);
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
 int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);
 
@@ -263,6 +270,7 @@ typedef struct cs_synth_config {
   int comm_priority;
   int host_source;        /* 1: gradients copied from pinned host memory each step */
   int p2p;                /* as cs_kv_config.p2p */
+  int grad_views;         /* 1: gradients are produced in place in the comm buckets (cs_kv_bucket_view) */
 } cs_synth_config;
 enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,

@@ -396,6 +396,23 @@ def create_communicators(transport: Transport, count: int) -> list[int]:
 
 # ----------------------------------------------------------------- kvstore
 
+class _CudaArray:
+    """__cuda_array_interface__ over a raw device pointer (zero-copy wrap)."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def device_tensor(ptr: int, numel: int, dtype: int | None, device: int = 0):
+    """A torch view of `numel` elements at device address `ptr` (memory owned
+    by the library, e.g. a KvStore bucket slot)."""
+    code = F32 if dtype is None else dtype
+    if code == BF16:  # no bf16 typestr: view 16-bit storage as bfloat16
+        return torch.as_tensor(_CudaArray(ptr, numel, "<i2"), device=f"cuda:{device}").view(torch.bfloat16)
+    return torch.as_tensor(_CudaArray(ptr, numel, {F32: "<f4", F64: "<f8"}[code]), device=f"cuda:{device}")
+
+
 @dataclass
 class KvConfig:
     """R/core/include/collsim/kvstore.hpp:26-30 + B200 extensions."""
@@ -484,6 +501,22 @@ class KvStore:
         check(lib.cs_kv_key_map(self.h, key, C.byref(b), C.byref(off)))
         return b.value, off.value
 
+    def bucket_view(self, key: int) -> int:
+        """Device address of the key's slot in its comm bucket (comm dtype)."""
+        p = C.c_void_p()
+        check(lib.cs_kv_bucket_view(self.h, key, C.byref(p)))
+        return p.value or 0
+
+    def bucket_view_tensor(self, key: int, numel: int, dtype: int, device: int = 0):
+        """The key's bucket slot as a torch tensor (zero-copy; dtype = the
+        comm dtype): produce the gradient into it and push it as the key's slot."""
+        return device_tensor(self.bucket_view(key), numel, dtype, device)
+
+    def arena(self) -> tuple[int, int]:
+        p, n = C.c_void_p(), C.c_uint64()
+        check(lib.cs_kv_arena(self.h, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
+
     def num_buckets(self) -> int:
         n = C.c_int()
         check(lib.cs_kv_num_buckets(self.h, C.byref(n)))
@@ -547,10 +580,10 @@ class SynthModel:
                  rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
                  backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0, p2p: bool = False,
                  host_source: bool = False, concom_comms: Sequence[int] = (),
-                 ready_ms: Sequence[float] | None = None):
+                 ready_ms: Sequence[float] | None = None, grad_views: bool = False):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
-                                int(fused_update), comm_priority, int(host_source), int(p2p))
+                                int(fused_update), comm_priority, int(host_source), int(p2p), int(grad_views))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()

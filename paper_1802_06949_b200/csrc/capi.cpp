@@ -556,6 +556,18 @@ int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems)
     kv->kv->key_map(key, bucket, offset_elems);
   });
 }
+int cs_kv_bucket_view(cs_kvstore_t kv, int key, void** ptr) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    *ptr = kv->kv->bucket_view(key);
+  });
+}
+int cs_kv_arena(cs_kvstore_t kv, void** base, uint64_t* bytes) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    kv->kv->arena(base, bytes);
+  });
+}
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out) {
   return guard([&] {
     CHECK_HANDLE(kv);
@@ -597,6 +609,7 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     c.comm_priority = cfg->comm_priority;
     c.host_source = cfg->host_source != 0;
     c.p2p = cfg->p2p;
+    c.grad_views = cfg->grad_views != 0;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
@@ -631,6 +644,7 @@ int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nran
     c.comm_priority = cfg->comm_priority;
     c.host_source = cfg->host_source != 0;
     c.p2p = cfg->p2p;
+    c.grad_views = cfg->grad_views != 0;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);

@@ -125,6 +125,19 @@ int KvStore::bucket_lane(int b) const {
   return buckets_[static_cast<size_t>(b)].lane;
 }
 
+void* KvStore::bucket_view(int key) {
+  check_key(key, true);
+  build_buckets();
+  return key_ptr(key);
+}
+
+void KvStore::arena(void** base, uint64_t* bytes) {
+  build_buckets();
+  if (!arena_) throw UsageError("KvStore: no fusion-bucket arena (bucket_bytes = 0 keeps one buffer per key)");
+  *base = arena_;
+  *bytes = arena_bytes_;
+}
+
 std::vector<std::vector<int>> KvStore::bucket_groups() {
   build_buckets();
   std::vector<std::vector<int>> g;
@@ -232,6 +245,8 @@ void KvStore::build_buckets() {
     arena = static_cast<char*>(device_alloc_zeroed(total * es));
     allocations_.push_back(arena);
   }
+  arena_ = arena;
+  arena_bytes_ = total * es;
   uint64_t off = 0;
   for (size_t i = 0; i < bs.size(); ++i) {
     Bucket& b = bs[i];
@@ -304,7 +319,8 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
       const TensorSlot& g = grads[static_cast<size_t>(i)];
       if (src_dt < 0) src_dt = g.dtype;
       if (g.dtype != src_dt) throw UsageError("KvStore: one push mixes gradient dtypes in a bucket");
-      entries.push_back(cs_copy_entry{g.data, key_ptr(k), g.numel});
+      if (g.data == key_ptr(k) && g.dtype == comm_dt_) B.view_tags.push_back(g.tag);  // in place
+      else entries.push_back(cs_copy_entry{g.data, key_ptr(k), g.numel});
       reads.push_back(g.tag);
       keys_[static_cast<size_t>(k)].pushed = true;
     }
@@ -315,7 +331,7 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
     DeviceTable* tab = B.pack_tab.get();  // resident table; all its launches on pack_lane_
     engine_.push_stream(
         [entries, src_dt, dst_dt, tab](cudaStream_t s) {
-          tab->pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
+          if (!entries.empty()) tab->pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
         },
         reads, muts, OpKind::Copy, key0, pack_lane_, Dispatch::Inline);
     B.pushed += static_cast<int>(idxs.size());
@@ -329,23 +345,9 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
 void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
   Bucket& B = buckets_[static_cast<size_t>(b)];
   std::vector<Tag> muts{B.tag};
-  Transport* tr = &transport_;
-  const int rank = rank_;
+  for (const Tag& t : B.view_tags) muts.push_back(t);  // rewritten in place
   const int key0 = B.keys[0];
-  const int bid = cfg_.bucket_bytes ? b : -1;
-  void* base = B.base;
-  const uint64_t count = B.count;
-  const int comm = B.comm;
-  const int dt = comm_dt_;
   B.issued = true;
-  (void)tr;
-  (void)base;
-  (void)count;
-  (void)dt;
-  (void)comm;
-  (void)rank;
-  (void)key0;
-  (void)bid;
   KvStore* self = this;
   if (cfg_.mode == KvMode::Funnel) {
     // control-thread collective on the single ordered comm stream
@@ -357,7 +359,10 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
     // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136)
     std::atomic<int>* outstanding = &outstanding_;
     outstanding_.fetch_add(1);
-    std::vector<Tag> reads = extra_reads;
+    std::vector<Tag> reads;
+    for (const Tag& t : extra_reads)
+      if (std::none_of(B.view_tags.begin(), B.view_tags.end(), [&](const Tag& v) { return v.id == t.id; }))
+        reads.push_back(t);
     engine_.push_stream(
         [self, b, outstanding](cudaStream_t s) {
           struct Drain {
@@ -434,6 +439,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     if (B.pushed != static_cast<int>(B.keys.size()))
       throw UsageError("KvStore: pull of a fusion bucket before all of its keys were pushed");
     std::vector<Tag> buf_tags{B.tag}, out_tags;
+    for (const Tag& t : B.view_tags) buf_tags.push_back(t);
     std::vector<cs_copy_entry> copies;
     std::vector<cs_update_entry> updates;
     int out_dt = -1;
@@ -442,6 +448,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       const TensorSlot& o = outs[static_cast<size_t>(i)];
       if (out_dt < 0) out_dt = o.dtype;
       if (o.dtype != out_dt) throw UsageError("KvStore: one pull mixes output dtypes in a bucket");
+      if (!sgd && o.data == key_ptr(k) && o.dtype == comm_dt_) continue;  // a bucket view: already in place
       out_tags.push_back(o.tag);
       if (sgd) {
         if (momentum) ensure_momentum(k, o.dtype);
@@ -462,7 +469,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     auto finish = [copies, updates, cdt, out_dt, opt, upd, utab, ctab](cudaStream_t s) {
       if (upd) utab->sgd(updates.data(), static_cast<int>(updates.size()), out_dt, cdt, opt.lr,
                          opt.rescale, opt.momentum, s);
-      else ctab->pack(copies.data(), static_cast<int>(copies.size()), cdt, out_dt, s);
+      else if (!copies.empty()) ctab->pack(copies.data(), static_cast<int>(copies.size()), cdt, out_dt, s);
     };
     const int key0 = keys[static_cast<size_t>(idxs[0])];
 
@@ -474,6 +481,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       // and carries the dummy tag, so collectives stay chained in push order;
       // the copy-out / update follows as an op on the update lane.
       std::vector<Tag> muts{B.tag};
+      for (const Tag& t : B.view_tags) muts.push_back(t);  // rewritten in place
       if (cfg_.mode == KvMode::DepCha) muts.push_back(dummy_tag_);
       const int ckey = B.keys[0];
       B.issued = true;
@@ -516,6 +524,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
           B.pushed = 0;
           B.pulled = 0;
           B.issued = false;
+          B.view_tags.clear();
         }
         continue;
       }
@@ -530,6 +539,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       B.pushed = 0;
       B.pulled = 0;
       B.issued = false;
+      B.view_tags.clear();
     }
   }
 }

@@ -96,6 +96,13 @@ class KvStore {
   int bucket_lane(int b) const;
   // Keys of every comm bucket, buckets in issue order (builds the map).
   std::vector<std::vector<int>> bucket_groups();
+  // Bucket views (DDP's gradient-as-bucket-view): the device address of the
+  // key's slot in its comm bucket, in the comm dtype.  A gradient produced
+  // there and pushed with that address is not copied (push only orders it);
+  // the collective then rewrites it in place.  Builds the buckets.
+  void* bucket_view(int key);
+  // The fusion-bucket arena (one allocation holding every bucket).
+  void arena(void** base, uint64_t* bytes);
 
  private:
   struct KeyState {
@@ -120,6 +127,10 @@ class KvStore {
     std::shared_ptr<DeviceTable> pack_tab, upd_tab, unpack_tab, p2p_tab;  // resident kernel tables
     std::vector<void*> peer_bufs;  // p2p: this bucket on every rank (IPC-mapped)
     void* mc = nullptr;            // nvls: this bucket's multicast VA
+    // tags of pushed gradients that ARE this bucket's slots (bucket views):
+    // the collective mutates them and the copy-out / update reads them, so a
+    // producer's next write waits for both
+    std::vector<Tag> view_tags;
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -158,6 +169,8 @@ class KvStore {
   bool built_ = false;
   bool p2p_active_ = false;
   NvlsBuffer nvls_;  // p2p == 2: the multicast-bound comm arena
+  void* arena_ = nullptr;
+  uint64_t arena_bytes_ = 0;
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call
   uint32_t stamp_ = 0;
   uint32_t next_stamp() {

@@ -177,6 +177,30 @@ void SynthModel::init() {
     kv_.init(k, TensorSlot{w_[k], cfg_.wdt, cfg_.sizes[k], wt_[k]});
   engine_.wait_all();
   groups_ = kv_.bucket_groups();
+  h2d_dst_ = g_arena_;
+  if (cfg_.grad_views) {
+    if (cfg_.bucket_bytes == 0) throw ConfigError("synth: bucket views need fusion buckets");
+    if (kv_.comm_dtype() != cfg_.gdt) throw ConfigError("synth: bucket views need comm dtype == gradient dtype");
+    void* base = nullptr;
+    uint64_t bytes = 0;
+    kv_.arena(&base, &bytes);
+    for (int k = 0; k < K; ++k) g_[k] = kv_.bucket_view(k);
+    if (cfg_.host_source) {
+      // the pinned source in bucket layout: one H2D copy fills every view
+      char* h = nullptr;
+      CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), bytes, cudaHostAllocDefault));
+      std::memset(h, 0, bytes);
+      for (int k = 0; k < K; ++k)
+        std::memcpy(h + (static_cast<char*>(g_[k]) - static_cast<char*>(base)), src_arena_ + goff[k],
+                    cfg_.sizes[k] * gs);
+      cudaFreeHost(src_arena_);
+      src_arena_ = h;
+      g_arena_bytes_ = bytes;
+    }
+    h2d_dst_ = base;
+    cudaFree(g_arena_);
+    g_arena_ = nullptr;
+  }
 }
 
 void SynthModel::enqueue_step(int flags) {
@@ -185,7 +209,7 @@ void SynthModel::enqueue_step(int flags) {
   if ((flags & kStepBackward) && cfg_.host_source) {
     // e2e input upload: the step's gradients arrive from pinned host memory
     // in one H2D copy of the contiguous gradient arena
-    void* dst = g_arena_;
+    void* dst = h2d_dst_;
     const void* src = src_arena_;
     const size_t bytes = g_arena_bytes_;
     engine_.push_stream(

@@ -36,6 +36,7 @@ struct SynthConfig {
   int comm_priority = 0;
   bool host_source = false;  // gradients arrive from pinned host memory (e2e)
   int p2p = 0;               // NVLink peer-memory collectives (KvConfig::p2p)
+  bool grad_views = false;   // produce gradients in place in the comm buckets (KvStore::bucket_view)
   uint64_t seed_base = 1000;
   // Measured gradient-ready time of every key from the start of a real
   // backward (tools/calibrate_backward.py).  When set, producers run in
@@ -85,6 +86,7 @@ class SynthModel {
   char* g_arena_ = nullptr;
   uint64_t g_arena_bytes_ = 0;
   char* src_arena_ = nullptr;  // device (synthetic) or pinned host (e2e)
+  void* h2d_dst_ = nullptr;    // e2e upload target: the gradient arena, or the bucket arena (views)
   double* sum_dev_ = nullptr;
   double* sum_host_ = nullptr;
   Tag sum_tag_;

@@ -8,7 +8,10 @@ the producer is PyTorch autograd on its own CUDA stream:
 
 * every parameter is a key (``model.parameters()`` order, like the
   reference's key = layer index); the gradients live in one flat arena with
-  256-B aligned slots so their device pointers never change;
+  256-B aligned slots so their device pointers never change -- or, with
+  ``bucket_views=True``, directly in the KvStore's comm buckets
+  (gradient-as-bucket-view: push copies nothing; after step() the gradient
+  buffers hold aggregation results, not this rank's gradient);
 * a post-accumulate-grad hook counts ready gradients per fusion bucket; when a
   bucket is complete it records a CUDA event on the autograd stream,
   ``Engine.import_event`` turns it into the latest write of the gradients
@@ -46,7 +49,7 @@ class TorchKvStoreDP:
     def __init__(self, model: torch.nn.Module, engine: api.Engine, transport: api.Transport, rank: int,
                  world: int, *, mode: str = "depcha", lr: float = 0.1, momentum: float = 0.0,
                  rescale: float | None = None, bucket_mb: float = 25.0, p2p: int = 1, outstanding: int = 1,
-                 concom_comms: Sequence[int] = (), comm_dtype: int = -1):
+                 concom_comms: Sequence[int] = (), comm_dtype: int = -1, bucket_views: bool = False):
         if mode not in ("depcha", "funnel"):
             raise ValueError("TorchKvStoreDP drives the DepCha / Funnel schedules (push during backward, "
                              "pull after it)")
@@ -66,18 +69,20 @@ class TorchKvStoreDP:
             raise ValueError("parameters must share one dtype")
         K = len(self.params)
 
-        # flat gradient arena: stable pointers, one memset to zero
+        if bucket_views and (bucket_mb <= 0 or comm_dtype not in (-1, api.dtype_code(dt))):
+            raise ValueError("bucket views need fusion buckets and comm dtype == parameter dtype")
         esz = torch.tensor([], dtype=dt).element_size()
-        offs, off = [], 0
-        for p in self.params:
-            offs.append(off)
-            off += (p.numel() * esz + _ALIGN - 1) // _ALIGN * _ALIGN // esz
-        self.grad_arena = torch.zeros(max(off, 1), dtype=dt, device=dev)
-        for p, o in zip(self.params, offs):
-            p.grad = self.grad_arena[o:o + p.numel()].view_as(p)
+        if not bucket_views:
+            # flat gradient arena: stable pointers, one memset to zero
+            offs, off = [], 0
+            for p in self.params:
+                offs.append(off)
+                off += (p.numel() * esz + _ALIGN - 1) // _ALIGN * _ALIGN // esz
+            self.grad_arena = torch.zeros(max(off, 1), dtype=dt, device=dev)
+            for p, o in zip(self.params, offs):
+                p.grad = self.grad_arena[o:o + p.numel()].view_as(p)
 
         self.w_slots = [api.Slot(p.data, engine.new_variable()) for p in self.params]
-        self.g_slots = [api.Slot(p.grad, engine.new_variable()) for p in self.params]
         cfg = api.KvConfig(mode, outstanding, K, comm_dtype=comm_dtype,
                            bucket_bytes=int(bucket_mb * 2**20), issue_order=1, comm_priority=-5,
                            p2p=p2p if world > 1 else 0)
@@ -89,6 +94,15 @@ class TorchKvStoreDP:
         groups: dict[int, list[int]] = {}
         for k in range(K):
             groups.setdefault(self.kv.key_map(k)[0], []).append(k)
+        if bucket_views:
+            # DDP's gradient_as_bucket_view: autograd accumulates straight into
+            # the comm buckets, so push copies nothing
+            base, nbytes = self.kv.arena()
+            self.grad_arena = api.device_tensor(base, nbytes // esz, api.dtype_code(dt), dev.index)
+            self.grad_arena.zero_()
+            for k, p in enumerate(self.params):
+                p.grad = self.kv.bucket_view_tensor(k, p.numel(), api.dtype_code(dt), dev.index).view_as(p)
+        self.g_slots = [api.Slot(p.grad, engine.new_variable()) for p in self.params]
         self.bucket_of = [0] * K
         self.groups = list(groups.values())
         for gi, keys in enumerate(self.groups):

@@ -619,3 +619,72 @@ def test_fusion_buckets_match_unbucketed(gpu, mode, comm_dtype):
         tol = 1e-6 if cdt == api.F32 else 1e-2
         scale = np.abs(w0) + 0.1 * 0.01 * np.sum([np.abs(x) for x in g], axis=0)
         assert np.all(np.abs(results[bucket_bytes][0][k] - ew) <= tol * scale + 1e-7)
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+@pytest.mark.parametrize("bucket_bytes", [0, 16 * 1024])
+@pytest.mark.parametrize("fused", [False, True])
+def test_bucket_views_train_steps_bit_exact(gpu, mode, bucket_bytes, fused):
+    """Gradients produced in place in the comm buckets (KvStore.bucket_view,
+    DDP's gradient-as-bucket-view): push copies nothing, the collective
+    rewrites the views, pull into the view itself is a no-op -- and the
+    weights after 3 iterations are still the reference KvStore's, bit for
+    bit (golden: tests/golden/train_steps.npz)."""
+    gold = np.load(GOLD / "train_steps.npz")
+    sizes = [int(s) for s in gold["sizes"]]
+    lr = float(gold["lr"])
+    K, R = len(sizes), 2
+    rescale = 1.0 / (64 * R)
+    outstanding = 2 if mode == "concom" else 1
+    transport = Transport.local(R, 10000)
+    finals = [[None] * K for _ in range(R)]
+
+    def body(rank, eng, store):
+        ws = [slot(eng, t64(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n)))
+              for k, n in enumerate(sizes)]
+        src = [t64(O.random_uniform(n, 1000 + rank * K + k)) for k, n in enumerate(sizes)]
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        gs = [slot(eng, store.bucket_view_tensor(k, n, api.F64, 0)) for k, n in enumerate(sizes)]
+        groups = {}
+        for k in range(K):
+            groups.setdefault(store.key_map(k)[0], []).append(k)
+        groups = [groups[b] for b in sorted(groups)]  # one push / pull per bucket
+        for _ in range(3):
+            for k in reversed(range(K)):
+                producer(eng, src[k], gs[k], k)
+            if mode in ("funnel", "concom"):
+                since = 0
+                for keys in groups:
+                    store.push(keys, [gs[k] for k in keys])
+                    if fused:
+                        store.pull_update(keys, [ws[k] for k in keys], lr, rescale)
+                    else:
+                        store.pull(keys, [gs[k] for k in keys])
+                        for k in keys:
+                            sgd_op(eng, ws[k], gs[k], lr, rescale, k)
+                    if mode == "concom":
+                        since += 1
+                        if since == outstanding:
+                            store.barrier()
+                            since = 0
+                if mode == "concom" and since:
+                    store.barrier()
+            else:
+                store.push(list(range(K)), gs)
+                if fused:
+                    store.pull_update(list(range(K)), ws, lr, rescale)
+                else:
+                    for k in range(K):
+                        store.pull(k, gs[k])
+                        sgd_op(eng, ws[k], gs[k], lr, rescale, k)
+            eng.wait_all()
+        for k in range(K):
+            finals[rank][k] = ws[k].value.cpu().numpy()
+
+    cfg = KvConfig(mode, outstanding, K, bucket_bytes=bucket_bytes, issue_order=1 if bucket_bytes else 0)
+    kv_ranks(R, 4, cfg, transport, None, body)
+    for r in range(R):
+        for k in range(K):
+            np.testing.assert_array_equal(finals[r][k], gold[f"{mode}_R{R}_r{r}_k{k}"])

@@ -82,3 +82,34 @@ def test_torch_producer_requires_every_gradient(gpu):
     dp.close()
     eng.close()
     tr.close()
+
+
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_torch_producer_bucket_views(gpu, momentum):
+    """bucket_views=True: autograd accumulates straight into the comm buckets
+    (no pack copy); the weights are still the oracle update bit for bit."""
+    model = _mlp(3)
+    eng = Engine(2, 0, None, 0)
+    tr = Transport.local(1, 5000)
+    lr, rescale = 0.05, 0.5
+    dp = TorchKvStoreDP(model, eng, tr, 0, 1, lr=lr, momentum=momentum, rescale=rescale, bucket_mb=0.1,
+                        bucket_views=True)
+    mom = np.zeros(sum(p.numel() for p in dp.params), np.float32)
+    w = _flat(dp.params)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    for step in range(3):
+        x = torch.randn(32, 64, device="cuda", generator=gen)
+        y = torch.randint(0, 10, (32,), device="cuda", generator=gen)
+        dp.zero_grad()
+        torch.nn.functional.cross_entropy(model(x), y).backward()
+        g = None
+        dp.step()
+        torch.cuda.synchronize()
+        g = _flat([p.grad for p in dp.params])  # 1 rank: the in-place "sum" is the gradient itself
+        w, mom = O.sgd_update(w, g, lr, rescale, momentum, mom if momentum else None, kind="f32")
+        if mom is None:
+            mom = np.zeros_like(w)
+        np.testing.assert_array_equal(_flat(dp.params), w, err_msg=f"step {step}")
+    dp.close()
+    eng.close()
+    tr.close()

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--channels-last", action="store_true")
     ap.add_argument("--metrics-out", default=None, help="write collsim-metrics-v1 (rank 0)")
+    ap.add_argument("--bucket-views", action="store_true", help="gradients accumulate in the comm buckets")
     a = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -80,11 +81,12 @@ def main():
             dist.broadcast_object_list(name, src=0)
             transport = api.Transport.nccl(name[0], world, rank, local, 120000)
             dp = TorchKvStoreDP(model, engine, transport, rank, world, lr=a.lr, momentum=a.momentum,
-                                bucket_mb=a.bucket_mb, p2p=1 if a.comm == "p2p" else 0)
+                                bucket_mb=a.bucket_mb, p2p=1 if a.comm == "p2p" else 0,
+                                bucket_views=a.bucket_views)
         else:
             transport = api.Transport.local(1, 120000)
             dp = TorchKvStoreDP(model, engine, transport, 0, 1, lr=a.lr, momentum=a.momentum,
-                                rescale=1.0 / world, bucket_mb=a.bucket_mb)
+                                rescale=1.0 / world, bucket_mb=a.bucket_mb, bucket_views=a.bucket_views)
 
         def step():
             dp.zero_grad()
@@ -139,6 +141,7 @@ def main():
                           "n_gpus": world, "batch_per_gpu": a.batch, "ms_per_step": round(ms, 3),
                           "images_per_s": round(world * a.batch / ms * 1e3, 1), "bucket_mb": a.bucket_mb,
                           "momentum": a.momentum, "channels_last": a.channels_last,
+                          "bucket_views": a.bucket_views,
                           "buckets": len(dp.groups) if dp else None, "steps": a.steps, "warmup": a.warmup,
                           "data": "synthetic random images, random-init torchvision resnet50, fp32/TF32"}),
               flush=True)
