@@ -242,8 +242,8 @@ def main():
               else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"}
     if args.impl == "reference":
         return reference_main(args, args.config, keys, mode, outstanding, config)
-    if args.comm is None:
-        args.comm = "nccl" if mode == "concom" else "p2p"
+    if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
+        args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
 
     import torch
     import torch.distributed as dist

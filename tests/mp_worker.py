@@ -95,9 +95,13 @@ def main():
                 store.pull_update(list(range(K)), ws, lr, rescale)
             else:
                 since = 0
-                for k in range(K):
-                    store.push(k, gs[k])
-                    store.pull_update(k, ws[k], lr, rescale)
+                groups = {}
+                for k in range(K):  # one push / pull per fusion bucket (1:1 without buckets)
+                    groups.setdefault(store.key_map(k)[0], []).append(k)
+                for b in sorted(groups):
+                    keys = groups[b]
+                    store.push(keys, [gs[k] for k in keys])
+                    store.pull_update(keys, [ws[k] for k in keys], lr, rescale)
                     if case_mode == "concom":
                         since += 1
                         if since == outstanding:

@@ -87,20 +87,23 @@ def test_nccl_schedules_match_reference(two_gpus, tmp_path, mode):
                     [s for s in outs[0]["trace"] if s.split(":")[1] == comm]
 
 
-def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path):
-    """DepCha over the NVLink peer-memory path: one fused allreduce+SGD kernel
-    per bucket (16 KiB fusion buckets).  Rank-order sums make the result
-    bit-identical to the reference KvStore at every world size."""
+@pytest.mark.parametrize("mode", ["depcha", "funnel"])
+def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path, mode):
+    """DepCha / Funnel over the NVLink peer-memory path: one fused
+    allreduce+SGD kernel per bucket (16 KiB fusion buckets).  Rank-order sums
+    make the result bit-identical to the reference KvStore at every world
+    size."""
     gold = np.load(HERE / "golden" / "train_steps.npz")
     K = len(gold["sizes"])
+    case = f"{mode}_p2p"
     for R in world_sizes(two_gpus):
         d = tmp_path / f"R{R}"
         d.mkdir()
-        outs = run_case("depcha_p2p", R, d)
+        outs = run_case(case, R, d)
         for r in range(R):
-            w = np.load(d / f"depcha_p2p_r{r}.npz")
+            w = np.load(d / f"{case}_r{r}.npz")
             for k in range(K):
-                np.testing.assert_array_equal(w[f"arr_{k}"], gold[f"depcha_R{R}_r{r}_k{k}"])
+                np.testing.assert_array_equal(w[f"arr_{k}"], gold[f"{mode}_R{R}_r{r}_k{k}"])
         for r in range(1, R):
             assert outs[r]["trace"] == outs[0]["trace"]
 
