@@ -83,6 +83,9 @@ def parse():
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--no-zero", dest="zero", action="store_false",
+                   help="replicated optimizer state instead of ZeRO-1 (the fused kernel's default at N>1: "
+                        "sharded master weights + momentum, weight all-gather, bit-identical results)")
     p.add_argument("--grad-views", action="store_true",
                    help="gradients produced in place in the comm buckets (gradient-as-bucket-view): "
                         "push copies nothing")
@@ -244,6 +247,9 @@ def main():
         return reference_main(args, args.config, keys, mode, outstanding, config)
     if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
         args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
+    config["optimizer_state"] = ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
+                                 "fused kernel" if (args.zero and args.comm == "p2p" and world > 1)
+                                 else "replicated on every rank")
 
     import torch
     import torch.distributed as dist
@@ -277,7 +283,8 @@ def main():
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
-                  p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views)
+                  p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
+                  zero=args.zero and args.comm == "p2p")
     config["collectives"] = ("identity (1 rank)" if world == 1 else
                              {"nccl": "NCCL",
                               "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",

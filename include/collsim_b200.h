@@ -213,6 +213,9 @@ typedef struct cs_kv_config {
   int p2p;               /* 1: NVLink peer-memory collectives (needs bucket_bytes > 0 and a
                             peer-capable NCCL transport); DepCha pull_update becomes one fused
                             allreduce+update kernel per bucket, rank-order (bit-exact) sums */
+  int zero;              /* 1 (with p2p = 1): ZeRO-1 -- each rank keeps master weights and momentum of
+                            its shard only; the fused kernel reduce-scatters, updates the shard and
+                            all-gathers the weights.  pull_update must cover whole buckets. */
 } cs_kv_config;
 typedef struct cs_slot { /* TensorSlot (kvstore.hpp:16-19): non-owning device view + tag */
   void* data;
@@ -271,6 +274,7 @@ typedef struct cs_synth_config {
   int host_source;        /* 1: gradients copied from pinned host memory each step */
   int p2p;                /* as cs_kv_config.p2p */
   int grad_views;         /* 1: gradients are produced in place in the comm buckets (cs_kv_bucket_view) */
+  int zero;               /* as cs_kv_config.zero */
 } cs_synth_config;
 enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,

@@ -424,6 +424,7 @@ class KvConfig:
     issue_order: int = 0
     comm_priority: int = 0
     p2p: int = 0
+    zero: int = 0
 
 
 @dataclass
@@ -445,7 +446,7 @@ class KvStore:
         cfg = _lib.KvConfigC(MODES[config.mode] if isinstance(config.mode, str) else config.mode,
                              config.outstanding, config.num_keys, config.comm_dtype,
                              config.bucket_bytes, config.issue_order, config.comm_priority,
-                             int(config.p2p))
+                             int(config.p2p), int(config.zero))
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()
         check(lib.cs_kv_create(engine.h, transport.h, rank, C.byref(cfg), comms, len(concom_comms),
@@ -580,10 +581,11 @@ class SynthModel:
                  rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
                  backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0, p2p: bool = False,
                  host_source: bool = False, concom_comms: Sequence[int] = (),
-                 ready_ms: Sequence[float] | None = None, grad_views: bool = False):
+                 ready_ms: Sequence[float] | None = None, grad_views: bool = False, zero: bool = False):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
-                                int(fused_update), comm_priority, int(host_source), int(p2p), int(grad_views))
+                                int(fused_update), comm_priority, int(host_source), int(p2p), int(grad_views),
+                                int(zero))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()

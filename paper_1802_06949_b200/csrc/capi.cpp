@@ -484,6 +484,7 @@ int cs_kv_create(cs_engine_t e, cs_transport_t t, int rank, const cs_kv_config* 
     c.issue_order = cfg->issue_order;
     c.comm_priority = cfg->comm_priority;
     c.p2p = cfg->p2p;
+    c.zero = cfg->zero;
     std::vector<int> comms;
     for (int i = 0; i < n_comms; ++i) comms.push_back(concom_comms[i]);
     auto h = std::make_unique<cs_kvstore>();
@@ -610,6 +611,7 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     c.host_source = cfg->host_source != 0;
     c.p2p = cfg->p2p;
     c.grad_views = cfg->grad_views != 0;
+    c.zero = cfg->zero;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
@@ -645,6 +647,7 @@ int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nran
     c.host_source = cfg->host_source != 0;
     c.p2p = cfg->p2p;
     c.grad_views = cfg->grad_views != 0;
+    c.zero = cfg->zero;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);

@@ -284,9 +284,10 @@ struct PackParams {
 };
 
 // groups [lo, hi) of one entry, all threads of the CTA
-template <int SDT, int DDT>
+template <int SDT, int DDT, int NT = kThreads>
 __device__ __forceinline__ void pack_segment(const void* src, void* dst, uint64_t n, bool vec,
                                              uint64_t lo, uint64_t hi) {
+  constexpr int kThreads = NT;  // block size of the caller (the peer kernels use 512)
   using Acc = typename AccOf<SDT, DDT>::T;
   constexpr int U = 4;
   uint64_t q = lo + threadIdx.x;
@@ -552,6 +553,8 @@ struct P2PParams {
   uint32_t* flags[CS_MAX_RANKS];
   void* mc;  // NVLS: multicast VA of the bucket (bufs unused in phase 1)
   void* recv[CS_MAX_RANKS];  // push mode: every rank's receive area (nranks slots of slot_groups)
+  void* wm[CS_MAX_RANKS];    // ZeRO-1: every rank's master-weight shard (shard-local layout)
+  void* mom_b;               // ZeRO-1: this rank's momentum shard (shard-local layout)
   const DevEntry* tab;
   uint64_t groups, slot_groups;
   double step, mu;
@@ -810,6 +813,120 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __g
     for (int k = NVLS ? 0 : 1; k < p.nranks; ++k) update_shard((p.rank + k) % p.nranks);
     // shard_only: owners may repack their buckets only after every reader is done
     if (p.shard_only) pair_barrier(p, 2);
+  }
+}
+
+// ------------------------------------------------ ZeRO-1
+//
+// Reduce-scatter + sharded update + all-gather of the WEIGHTS in one
+// cooperative launch.  Rank r keeps the master weights and the momentum of
+// its shard only (shard-local layout, 1/N of the optimizer state):
+//   phase 1  CTA c sums chunk c of shard r over the N buckets (peer loads,
+//            rank order -- bit-identical sums) and, with the sum still in
+//            registers, applies the SGD / momentum update to the master
+//            shard (the same arithmetic as kernel (c) on the same values);
+//   phase 2  after the pair barrier, CTA c copies chunk c of every owner's
+//            updated master shard into this rank's weight tensors (peer
+//            loads, staggered owners), through the key table.
+// No trailing barrier: an owner rewrites its master only in the next launch,
+// after that launch's arrival barrier, which every reader reaches only once
+// this launch has finished on its GPU.
+
+template <int CDT, typename Acc>
+__device__ __forceinline__ Acc comm_rounded(Acc x) {  // the value the bucket would hold
+  if constexpr (CDT == CS_BF16) return __bfloat162float(__float2bfloat16_rn(x));
+  else return x;
+}
+
+template <int CDT, int WDT, bool MOM, int M>
+__device__ __forceinline__ void zero_reduce_update(const P2PParams& p, uint64_t s0, uint64_t a, uint64_t b) {
+  using CAcc = typename AccOf<CDT, CDT>::T;
+  using WAcc = typename AccOf<WDT, WDT>::T;
+  constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
+  const WAcc step = static_cast<WAcc>(p.step), mu = static_cast<WAcc>(p.mu);
+  const int m = (M > 0) ? M : p.nranks;
+  if (threadIdx.x >= kP2PLinkThreads) return;
+  void* wm = p.wm[p.rank];
+  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+    const uint64_t i = q * kVec, j = (q - s0) * kVec;  // bucket element / shard-local element
+    CAcc acc[kVec];
+    if constexpr (M > 0) {
+      CAcc x[M][kVec];
+#pragma unroll
+      for (int r = 0; r < M; ++r) load8_rw<CDT, CAcc>(p.bufs[r], i, x[r]);
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) acc[v] = x[0][v];
+#pragma unroll
+      for (int r = 1; r < M; ++r)
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) acc[v] = add_rn(acc[v], x[r][v]);
+    } else {
+      load8_rw<CDT, CAcc>(p.bufs[0], i, acc);
+      for (int r = 1; r < m; ++r) {
+        CAcc x[kVec];
+        load8_rw<CDT, CAcc>(p.bufs[r], i, x);
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) acc[v] = add_rn(acc[v], x[v]);
+      }
+    }
+    WAcc w[kVec], mv[kVec] = {};
+    load8_rw<WDT, WAcc>(wm, j, w);
+    if constexpr (MOM) load8_rw<MDT, WAcc>(p.mom_b, j, mv);
+#pragma unroll
+    for (int v = 0; v < kVec; ++v)
+      sgd_elem<MOM>(w[v], static_cast<WAcc>(comm_rounded<CDT>(acc[v])), mv[v], step, mu);
+    store8<WDT, WAcc>(wm, j, w);
+    if constexpr (MOM) store8<MDT, WAcc>(p.mom_b, j, mv);
+  }
+}
+
+// owner s's updated master weights, bucket groups [a, b) of its shard (which
+// starts at group s0), into this rank's weight tensors (table: c = weights)
+template <int WDT>
+__device__ __forceinline__ void zero_gather(const P2PParams& p, int s, uint64_t s0, uint64_t a, uint64_t b) {
+  if (a >= b || p.n_entries == 0) return;
+  constexpr uint64_t kElem = (WDT == CS_F64) ? 8 : 4;
+  int lo = 0, hi = p.n_entries;  // first entry with gend > a
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p.tab[mid].gend <= a) lo = mid + 1;
+    else hi = mid;
+  }
+  const uintptr_t shard_base = reinterpret_cast<uintptr_t>(p.wm[s]);
+  for (int e = lo; e < p.n_entries; ++e) {
+    const DevEntry en = p.tab[e];
+    if (en.gstart >= b) break;
+    const uint64_t g0 = max(a, en.gstart), g1 = min(b, en.gend);
+    // the key's element 0 sits at shard-local element (gstart - s0) * 8 (may
+    // precede the shard when the key straddles it; only [g0, g1) is touched)
+    const uintptr_t src = shard_base + (en.gstart * kVec - s0 * kVec) * kElem;
+    const bool vec = ((src | reinterpret_cast<uintptr_t>(en.c)) & 15u) == 0;
+    pack_segment<WDT, WDT, kP2PThreads>(reinterpret_cast<const void*>(src), en.c, en.n, vec, g0 - en.gstart,
+                                        g1 - en.gstart);
+  }
+}
+
+template <int CDT, int WDT, bool MOM, int M>
+__global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_constant__ P2PParams p) {
+  const uint64_t T = p.groups;
+  const uint64_t G = gridDim.x, c = blockIdx.x;
+  auto chunk = [&](int s, uint64_t& s0, uint64_t& a, uint64_t& b) {
+    s0 = T * s / p.nranks;
+    const uint64_t L = T * (s + 1) / p.nranks - s0;
+    a = s0 + L * c / G;
+    b = s0 + L * (c + 1) / G;
+  };
+  uint64_t s0, a, b;
+  pair_barrier(p, 0);
+  chunk(p.rank, s0, a, b);
+  zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b);
+  __syncthreads();
+  zero_gather<WDT>(p, p.rank, s0, a, b);  // own shard: no need to wait for the peers
+  pair_barrier(p, 1);
+  for (int k = 1; k < p.nranks; ++k) {
+    const int s = (p.rank + k) % p.nranks;
+    chunk(s, s0, a, b);
+    zero_gather<WDT>(p, s, s0, a, b);
   }
 }
 
@@ -1354,6 +1471,10 @@ const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cu
 
 size_t p2p_flag_bytes() { return sizeof(uint32_t) * 3 * CS_MAX_RANKS * kP2PMaxCtas; }
 
+uint64_t p2p_shard_elems(uint64_t count, int nranks) {
+  return (count / kVec + nranks - 1) / nranks * kVec;
+}
+
 size_t p2p_recv_bytes(uint64_t count, int cdt, int nranks) {
   const uint64_t slot_groups = (count / kVec + nranks - 1) / nranks;
   return static_cast<size_t>(nranks) * slot_groups * kVec * dtype_size(cdt);
@@ -1398,6 +1519,13 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   p.rank = a.rank;
   p.epoch = a.epoch;
   p.shard_only = (a.shard_only && a.update && !a.mc) ? 1 : 0;
+  const bool zero = a.zero && a.update && !a.mc;
+  if (a.zero && !zero) throw UsageError("p2p_allreduce: ZeRO-1 needs the fused update over peer memory");
+  for (int r = 0; zero && r < a.nranks; ++r) {
+    p.wm[r] = a.wm[r];
+    if (!aligned16(a.wm[r])) throw UsageError("p2p_allreduce: master shard not 16-byte aligned");
+  }
+  p.mom_b = a.mom_b;
   const int grid = p2p_grid(p.groups, a.nranks);
   const bool upd = a.update && a.tab && a.n_entries > 0;
   const bool mom = a.momentum != 0.0;
@@ -1460,6 +1588,25 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     CSB_NVLS_PICK(CS_BF16, CS_F32, true, false)
     CSB_NVLS_PICK(CS_BF16, CS_F32, true, true)
 #undef CSB_NVLS_PICK
+  }
+  if (zero) {
+    fn = nullptr;
+#define CSB_ZERO_PICK(C, W, MO)                                                                  \
+  if (a.cdt == C && a.wdt == W && mom == MO) {                                                   \
+    switch (a.nranks) {                                                                          \
+      case 2: fn = reinterpret_cast<const void*>(p2p_zero_kernel<C, W, MO, 2>); break;           \
+      case 4: fn = reinterpret_cast<const void*>(p2p_zero_kernel<C, W, MO, 4>); break;           \
+      case 8: fn = reinterpret_cast<const void*>(p2p_zero_kernel<C, W, MO, 8>); break;           \
+      default: fn = reinterpret_cast<const void*>(p2p_zero_kernel<C, W, MO, 0>); break;          \
+    }                                                                                            \
+  }
+    CSB_ZERO_PICK(CS_F32, CS_F32, false)
+    CSB_ZERO_PICK(CS_F32, CS_F32, true)
+    CSB_ZERO_PICK(CS_BF16, CS_F32, false)
+    CSB_ZERO_PICK(CS_BF16, CS_F32, true)
+    CSB_ZERO_PICK(CS_F64, CS_F64, false)
+    CSB_ZERO_PICK(CS_F64, CS_F64, true)
+#undef CSB_ZERO_PICK
   }
   if (!fn) throw UsageError("p2p_allreduce: unsupported dtype combination");
   CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));

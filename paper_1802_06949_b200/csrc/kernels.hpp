@@ -77,10 +77,17 @@ struct P2PArgs {
   int n_entries = 0;
   bool update = false;
   bool shard_only = false;  // phase 1 stores only the own shard; the update reads the owners' buckets
+  // ZeRO-1: master-weight shards of every rank and this rank's momentum shard
+  // (shard-local layout, p2p_shard_elems each); weights all-gathered after the update
+  bool zero = false;
+  void* wm[CS_MAX_RANKS] = {};
+  void* mom_b = nullptr;
   double lr = 0, rescale = 0, momentum = 0;
 };
 size_t p2p_flag_bytes();
 size_t p2p_recv_bytes(uint64_t count, int cdt, int nranks);
+// elements of the largest shard of a `count`-element bucket (a multiple of 8)
+uint64_t p2p_shard_elems(uint64_t count, int nranks);
 int p2p_grid(uint64_t groups, int nranks);
 void p2p_allreduce(const P2PArgs& args, cudaStream_t s);
 

@@ -72,8 +72,11 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   // hold the SMs the other needs on a peer, so ConCom stays on NCCL.
   if (cfg_.p2p && cfg_.mode == KvMode::ConCom)
     throw ConfigError("KvStore: the peer-memory path runs on one ordered comm stream (funnel/depcha)");
+  if (cfg_.zero && (cfg_.p2p != 1 || cfg_.mode == KvMode::ConCom || cfg_.mode == KvMode::Naive))
+    throw ConfigError("KvStore: ZeRO-1 runs on the peer-memory path (p2p = 1) under funnel/depcha");
   // one rank: nothing crosses NVLink, the collectives are the identity
   p2p_active_ = cfg_.p2p != 0 && transport_.p2p_capable();
+  zero_active_ = p2p_active_ && cfg_.zero;
   if (engine_.device() < 0) throw ConfigError("KvStore: the engine must be bound to a CUDA device");
   keys_.resize(static_cast<size_t>(cfg_.num_keys));
   init_order_tag_ = engine_.new_variable();
@@ -123,6 +126,25 @@ void KvStore::key_map(int key, int* bucket, uint64_t* offset) {
 int KvStore::bucket_lane(int b) const {
   if (b < 0 || b >= num_buckets()) throw UsageError("KvStore: bucket out of range");
   return buckets_[static_cast<size_t>(b)].lane;
+}
+
+// ZeRO-1: the first fused op of a bucket seeds this rank's master shard from
+// its (broadcast, identical) weights, on the op's stream before the kernel.
+void KvStore::zero_fill_master(Bucket& B, const std::vector<DeviceTable::Entry>& es, int wdt, cudaStream_t s) {
+  const int N = transport_.num_ranks();
+  const uint64_t T = B.count / 8, s0 = T * rank_ / N, s1 = T * (rank_ + 1) / N;
+  const uint64_t ws = dtype_size(wdt);
+  char* master = static_cast<char*>(const_cast<void*>(B.wm_peers[static_cast<size_t>(rank_)]));
+  std::vector<cs_copy_entry> copies;
+  for (const DeviceTable::Entry& e : es) {
+    const uint64_t g0 = std::max(e.gstart, s0), g1 = std::min(e.gend, s1);
+    if (g0 >= g1) continue;
+    const uint64_t e0 = (g0 - e.gstart) * 8, e1 = std::min<uint64_t>(e.n, (g1 - e.gstart) * 8);
+    if (e0 >= e1) continue;
+    copies.push_back(cs_copy_entry{static_cast<char*>(e.c) + e0 * ws, master + (g0 - s0) * 8 * ws, e1 - e0});
+  }
+  if (!copies.empty()) pack(copies.data(), static_cast<int>(copies.size()), wdt, wdt, s);
+  B.master_ready = true;
 }
 
 void* KvStore::bucket_view(int key) {
@@ -274,6 +296,28 @@ void KvStore::build_buckets() {
     for (Bucket& b : bs) {
       const uint64_t boff = static_cast<uint64_t>(static_cast<char*>(b.base) - arena);
       for (void* p : peers) b.peer_bufs.push_back(static_cast<char*>(p) + boff);
+    }
+  }
+  if (zero_active_) {
+    // ZeRO-1 shards: master weights (IPC-shared: peers all-gather from them)
+    // and momentum, each 1/N of the bucket, in shard-local layout
+    zero_wdt_ = keys_[0].wdtype;
+    for (const KeyState& k : keys_)
+      if (k.wdtype != zero_wdt_) throw UsageError("KvStore: ZeRO-1 needs one weight dtype for every key");
+    const uint64_t ws = dtype_size(zero_wdt_), ms = zero_wdt_ == CS_F64 ? 8 : 4;
+    const int N = transport_.num_ranks();
+    uint64_t shard_total = 0;
+    for (const Bucket& b : bs) shard_total += p2p_shard_elems(b.count, N);
+    void* master = device_alloc_zeroed(shard_total * ws);
+    void* mom = device_alloc_zeroed(shard_total * ms);
+    allocations_.push_back(master);
+    allocations_.push_back(mom);
+    const std::vector<void*> peers = transport_.share_buffer(master);
+    uint64_t soff = 0;
+    for (Bucket& b : bs) {
+      for (void* p : peers) b.wm_peers.push_back(static_cast<char*>(p) + soff * ws);
+      b.mom_b = static_cast<char*>(mom) + soff * ms;
+      soff += p2p_shard_elems(b.count, N);
     }
   }
   buckets_ = std::move(bs);
@@ -451,7 +495,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       if (!sgd && o.data == key_ptr(k) && o.dtype == comm_dt_) continue;  // a bucket view: already in place
       out_tags.push_back(o.tag);
       if (sgd) {
-        if (momentum) ensure_momentum(k, o.dtype);
+        if (momentum && !zero_active_) ensure_momentum(k, o.dtype);  // ZeRO-1 keeps a momentum shard
         updates.push_back(cs_update_entry{o.data, key_ptr(k), keys_[static_cast<size_t>(k)].mom, o.numel});
       } else {
         copies.push_back(cs_copy_entry{key_ptr(k), o.data, o.numel});
@@ -505,8 +549,12 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         // this op updates every key of the bucket, so nothing reads the
         // bucket afterwards: keep only the own shard of the sum locally
         const bool whole = B.pulled == 0 && idxs.size() == B.keys.size();
+        if (zero_active_ && (!whole || out_dt != zero_wdt_))
+          throw UsageError("KvStore: ZeRO-1 needs pull_update of whole fusion buckets into the init weights' dtype");
+        const bool zero = zero_active_;
         engine_.push_stream(
-            [self, bi, es, ptab, out_dt, opt, whole](cudaStream_t s) {
+            [self, bi, es, ptab, out_dt, opt, whole, zero](cudaStream_t s) {
+              Bucket& Bk = self->buckets_[bi];
               Transport::P2PUpdate u;
               u.tab = ptab->resident(es, s);
               u.n_entries = static_cast<int>(es.size());
@@ -515,7 +563,12 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
               u.rescale = opt.rescale;
               u.momentum = opt.momentum;
               u.shard_only = whole;
-              self->collective_body(self->buckets_[bi], bi, s, &u);
+              if (zero) {
+                if (!Bk.master_ready) self->zero_fill_master(Bk, es, out_dt, s);
+                u.wm = Bk.wm_peers.data();
+                u.mom_b = Bk.mom_b;
+              }
+              self->collective_body(Bk, bi, s, &u);
             },
             {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
         for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;

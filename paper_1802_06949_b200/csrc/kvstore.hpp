@@ -47,6 +47,9 @@ struct KvConfig {
   // buckets and a peer-capable NCCL transport): bit-exact rank-order sums,
   // and DepCha's pull_update becomes ONE fused allreduce+update kernel.
   int p2p = 0;
+  // ZeRO-1 over the fused kernel (p2p == 1): master weights + momentum of the
+  // own shard only; the kernel all-gathers the updated weights.
+  int zero = 0;
 };
 
 // Non-owning device view + engine tag (kvstore.hpp:16-19).
@@ -131,6 +134,12 @@ class KvStore {
     // the collective mutates them and the copy-out / update reads them, so a
     // producer's next write waits for both
     std::vector<Tag> view_tags;
+    // ZeRO-1: every rank's master-weight shard of this bucket, this rank's
+    // momentum shard (shard-local layout), filled from the weights at the
+    // first pull_update
+    std::vector<const void*> wm_peers;
+    void* mom_b = nullptr;
+    bool master_ready = false;
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -148,6 +157,7 @@ class KvStore {
   // CSB_DEPCHA_DISPATCH=pool restores the reference's pool dispatch.
   Dispatch depcha_dispatch() const;
   void collective_body(const Bucket& B, int bucket_id, cudaStream_t s, const Transport::P2PUpdate* upd);
+  void zero_fill_master(Bucket& B, const std::vector<DeviceTable::Entry>& es, int wdt, cudaStream_t s);
 
   Engine& engine_;
   Transport& transport_;
@@ -171,6 +181,8 @@ class KvStore {
   NvlsBuffer nvls_;  // p2p == 2: the multicast-bound comm arena
   void* arena_ = nullptr;
   uint64_t arena_bytes_ = 0;
+  bool zero_active_ = false;  // ZeRO-1 (cfg_.zero over an active peer-memory path)
+  int zero_wdt_ = -1;
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call
   uint32_t stamp_ = 0;
   uint32_t next_stamp() {

@@ -67,6 +67,7 @@ KvConfig kv_config(const SynthConfig& c) {
   k.issue_order = c.issue_order;
   k.comm_priority = c.comm_priority;
   k.p2p = c.p2p;
+  k.zero = c.zero;
   return k;
 }
 

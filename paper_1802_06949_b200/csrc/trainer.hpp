@@ -37,6 +37,7 @@ struct SynthConfig {
   bool host_source = false;  // gradients arrive from pinned host memory (e2e)
   int p2p = 0;               // NVLink peer-memory collectives (KvConfig::p2p)
   bool grad_views = false;   // produce gradients in place in the comm buckets (KvStore::bucket_view)
+  int zero = 0;              // ZeRO-1 sharded update (KvConfig::zero)
   uint64_t seed_base = 1000;
   // Measured gradient-ready time of every key from the start of a real
   // backward (tools/calibrate_backward.py).  When set, producers run in

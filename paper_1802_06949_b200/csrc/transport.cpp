@@ -263,6 +263,11 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     a.rescale = upd->rescale;
     a.momentum = upd->momentum;
     a.shard_only = upd->shard_only && !mc;
+    if (upd->wm) {
+      a.zero = true;
+      for (int r = 0; r < num_ranks(); ++r) a.wm[r] = const_cast<void*>(upd->wm[r]);
+      a.mom_b = upd->mom_b;
+    }
   }
   device_latency(stream);
   p2p_allreduce(a, stream);

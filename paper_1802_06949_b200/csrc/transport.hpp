@@ -79,6 +79,8 @@ class Transport {
     int wdt = CS_F32;
     double lr = 0, rescale = 0, momentum = 0;
     bool shard_only = false;  // the bucket keeps only this rank's shard (update reads owners)
+    const void* const* wm = nullptr;  // ZeRO-1: every rank's master shard; null = replicated update
+    void* mom_b = nullptr;            // ZeRO-1: this rank's momentum shard
   };
   // Allreduce of one bucket through peer memory, matched by the ledger like
   // allreduce_sum; with `upd`, fused with the SGD / momentum update of the

@@ -49,7 +49,8 @@ class TorchKvStoreDP:
     def __init__(self, model: torch.nn.Module, engine: api.Engine, transport: api.Transport, rank: int,
                  world: int, *, mode: str = "depcha", lr: float = 0.1, momentum: float = 0.0,
                  rescale: float | None = None, bucket_mb: float = 25.0, p2p: int = 1, outstanding: int = 1,
-                 concom_comms: Sequence[int] = (), comm_dtype: int = -1, bucket_views: bool = False):
+                 concom_comms: Sequence[int] = (), comm_dtype: int = -1, bucket_views: bool = False,
+                 zero: bool = False):
         if mode not in ("depcha", "funnel"):
             raise ValueError("TorchKvStoreDP drives the DepCha / Funnel schedules (push during backward, "
                              "pull after it)")
@@ -85,7 +86,7 @@ class TorchKvStoreDP:
         self.w_slots = [api.Slot(p.data, engine.new_variable()) for p in self.params]
         cfg = api.KvConfig(mode, outstanding, K, comm_dtype=comm_dtype,
                            bucket_bytes=int(bucket_mb * 2**20), issue_order=1, comm_priority=-5,
-                           p2p=p2p if world > 1 else 0)
+                           p2p=p2p if world > 1 else 0, zero=int(zero and world > 1))
         self.kv = api.KvStore(engine, transport, rank, cfg, concom_comms)
         torch.cuda.synchronize(dev)  # the weights were written on the framework stream
         for k in range(K):

@@ -63,14 +63,15 @@ def main():
     elif case.split("_")[0] in ("funnel", "depcha", "concom"):
         mode = case.split("_")[0]
         split = case.endswith("_p2psplit")  # one pull_update per key: buckets not whole
-        p2p = case.endswith("_p2p") or split
+        zero = case.endswith("_p2pzero")  # ZeRO-1: sharded master weights + all-gather
+        p2p = case.endswith("_p2p") or split or zero
         gold = np.load(HERE / "golden" / "train_steps.npz")
         sizes = [int(x) for x in gold["sizes"]]
         K, lr, rescale = len(sizes), float(gold["lr"]), 1.0 / (64 * world)
         outstanding = 2 if mode == "concom" else 1
         comms = create_communicators(tr, outstanding) if mode == "concom" else []
         eng = Engine(4, rank, sink, local)
-        cfg = KvConfig(mode, outstanding, K, bucket_bytes=16 * 1024 if p2p else 0, p2p=int(p2p))
+        cfg = KvConfig(mode, outstanding, K, bucket_bytes=16 * 1024 if p2p else 0, p2p=int(p2p), zero=int(zero))
         store = KvStore(eng, tr, rank, cfg, comms)
         case_mode = mode
         ws = [Slot(t64(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n), dev),
@@ -140,14 +141,15 @@ def main():
             res[f"w{so}"], res[f"m{so}"], res[f"buf{so}"] = w.cpu().numpy(), m.cpu().numpy(), buf.cpu().numpy()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)
         eng.close()
-    elif case == "torch_dp":
+    elif case in ("torch_dp", "torch_dp_zero"):
         # real-backward producer over the fused NVLink kernel: save every
         # rank's per-step gradients and weights; the test replays the oracle
         from paper_1802_06949_b200.torch_dp import TorchKvStoreDP
         torch.manual_seed(0)
         model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).to(dev)
         eng = Engine(4, rank, sink, local)
-        dp = TorchKvStoreDP(model, eng, tr, rank, world, lr=0.05, momentum=0.9, bucket_mb=0.05, p2p=1)
+        dp = TorchKvStoreDP(model, eng, tr, rank, world, lr=0.05, momentum=0.9, bucket_mb=0.05, p2p=1,
+                            zero=case == "torch_dp_zero")
         flat = lambda ts: np.concatenate([t.detach().cpu().numpy().ravel() for t in ts])  # noqa: E731
         res = {"w0": flat(dp.params), "buckets": np.array(len(dp.groups))}
         gen = torch.Generator(device=dev).manual_seed(100 + rank)

@@ -87,15 +87,17 @@ def test_nccl_schedules_match_reference(two_gpus, tmp_path, mode):
                     [s for s in outs[0]["trace"] if s.split(":")[1] == comm]
 
 
-@pytest.mark.parametrize("mode", ["depcha", "funnel"])
-def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path, mode):
+@pytest.mark.parametrize("mode,variant", [("depcha", "p2p"), ("funnel", "p2p"), ("depcha", "p2pzero"),
+                                          ("funnel", "p2pzero")])
+def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path, mode, variant):
     """DepCha / Funnel over the NVLink peer-memory path: one fused
     allreduce+SGD kernel per bucket (16 KiB fusion buckets).  Rank-order sums
     make the result bit-identical to the reference KvStore at every world
-    size."""
+    size.  p2pzero: ZeRO-1 (each rank updates master weights of its shard
+    only, then the kernel all-gathers the weights) -- still bit-identical."""
     gold = np.load(HERE / "golden" / "train_steps.npz")
     K = len(gold["sizes"])
-    case = f"{mode}_p2p"
+    case = f"{mode}_{variant}"
     for R in world_sizes(two_gpus):
         d = tmp_path / f"R{R}"
         d.mkdir()
@@ -155,15 +157,17 @@ def test_p2p_c_abi_reduce_and_shard_only(two_gpus, tmp_path):
             np.testing.assert_array_equal(o["w0"], outs[0]["w0"])
 
 
-def test_torch_producer_over_nvlink_bit_exact(two_gpus, tmp_path):
+@pytest.mark.parametrize("case", ["torch_dp", "torch_dp_zero"])
+def test_torch_producer_over_nvlink_bit_exact(two_gpus, tmp_path, case):
     """PyTorch autograd as the producer (torch_dp.TorchKvStoreDP, 2-3 fusion
-    buckets, fused NVLink kernel): every rank's weights after each step are
-    the f32 oracle update with the rank-order sum of the ranks' gradients."""
+    buckets, fused NVLink kernel; torch_dp_zero: ZeRO-1 sharded momentum and
+    master weights): every rank's weights after each step are the f32 oracle
+    update with the rank-order sum of the ranks' gradients."""
     for R in world_sizes(two_gpus):
         d = tmp_path / f"R{R}"
         d.mkdir()
-        run_case("torch_dp", R, d)
-        outs = [np.load(d / f"torch_dp_r{r}.npz") for r in range(R)]
+        run_case(case, R, d)
+        outs = [np.load(d / f"{case}_r{r}.npz") for r in range(R)]
         assert int(outs[0]["buckets"]) >= 2
         w = outs[0]["w0"].astype(np.float32)
         mom = np.zeros_like(w)

@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--channels-last", action="store_true")
     ap.add_argument("--metrics-out", default=None, help="write collsim-metrics-v1 (rank 0)")
     ap.add_argument("--bucket-views", action="store_true", help="gradients accumulate in the comm buckets")
+    ap.add_argument("--zero", action="store_true", help="ZeRO-1 sharded optimizer state (kv, N>1)")
     a = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -82,7 +83,7 @@ def main():
             transport = api.Transport.nccl(name[0], world, rank, local, 120000)
             dp = TorchKvStoreDP(model, engine, transport, rank, world, lr=a.lr, momentum=a.momentum,
                                 bucket_mb=a.bucket_mb, p2p=1 if a.comm == "p2p" else 0,
-                                bucket_views=a.bucket_views)
+                                bucket_views=a.bucket_views, zero=a.zero)
         else:
             transport = api.Transport.local(1, 120000)
             dp = TorchKvStoreDP(model, engine, transport, 0, 1, lr=a.lr, momentum=a.momentum,
@@ -141,7 +142,7 @@ def main():
                           "n_gpus": world, "batch_per_gpu": a.batch, "ms_per_step": round(ms, 3),
                           "images_per_s": round(world * a.batch / ms * 1e3, 1), "bucket_mb": a.bucket_mb,
                           "momentum": a.momentum, "channels_last": a.channels_last,
-                          "bucket_views": a.bucket_views,
+                          "bucket_views": a.bucket_views, "zero": a.zero,
                           "buckets": len(dp.groups) if dp else None, "steps": a.steps, "warmup": a.warmup,
                           "data": "synthetic random images, random-init torchvision resnet50, fp32/TF32"}),
               flush=True)
