@@ -364,8 +364,12 @@ def main():
         if world > 1 and args.comm in ("p2p", "nvls") and dom == "sum":
             # the fused allreduce+update kernel is NVLink-bound: algorithmic
             # bytes crossing the link per GPU per direction, per step
-            # (peer loads: 2(N-1)/N x bucket bytes; NVLS: 1 x bucket bytes)
-            link_step = gbytes * (2.0 * (world - 1) / world if args.comm == "p2p" else 1.0)
+            # peer loads: (N-1)/N of the gradients in the reduce-scatter, plus
+            # (N-1)/N of the reduced gradients (replicated update) or of the
+            # fp32 master weights (ZeRO-1 all-gather); NVLS: 1 x bucket bytes
+            zero_on = args.zero and args.comm == "p2p"
+            second = sum(keys) * 4 if zero_on else gbytes
+            link_step = ((world - 1) / world * (gbytes + second) if args.comm == "p2p" else gbytes)
             bytes_launch = link_step * n_prof / max(1, ks["launches"])
             bound, peak = "nvlink", pk.get("nvlink_gbs_per_dir", 770.0)
             peak_source = ("MEASURED_PEAKS.json nvlink_gbs_per_dir" if "nvlink_gbs_per_dir" in pk else
