@@ -9,7 +9,7 @@ B200 run.  B200-only details go under an extra "b200" object, which the
 reference parser ignores.
 
 run_synthetic() is the run_scenario analogue: rank threads over the local
-transport (one process, ranks on GPUs r mod ngpus), each with its own engine
+transport (one process, the ranks sharing one GPU), each with its own engine
 and the native synthetic-backward trainer (trainer.cpp), with a trace sink.
 """
 from __future__ import annotations
@@ -120,11 +120,13 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
                   epochs: int = 2, steps_per_epoch: int = 3, sizes: Sequence[int] = (4096,) * 8,
                   bucket_bytes: int = 0, seed: int = 1, global_batch: int = 64, momentum: float = 0.0,
                   backward_ms: float = 0.0, watchdog_ms: int = 30000, model_name: str = "synthetic",
-                  trace_path: str | None = None, metrics_path: str | None = None) -> Metrics:
+                  trace_path: str | None = None, metrics_path: str | None = None, device: int = 0) -> Metrics:
     """runner.cpp:47-135 over the GPU path: validate, one transport + trace
     sink, communicators for ConCom, rank threads each running the native
     trainer loop shape, then the metrics (epoch wall time averaged over
-    workers, gauges from the sink, the primary error by priority)."""
+    workers, gauges from the sink, the primary error by priority).  The rank
+    threads share `device` (the reference's ranks share one host); one
+    process per GPU is the NCCL / NVLink transport's job."""
     from . import api
     if workers < 1:
         raise ConfigError(-1, "run: workers must be >= 1")
@@ -136,18 +138,18 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
         raise ConfigError(-1, "run: global batch size must divide evenly across workers")
     if mode == "concom" and outstanding < 1:
         raise ConfigError(-1, "run: concom requires outstanding >= 1")
-    ndev = max(1, api.device_count())
     sink = api.TraceSink()
     transport = api.Transport.local(workers, watchdog_ms, sink)
     comms = api.create_communicators(transport, outstanding) if mode == "concom" else []
     walls = [[] for _ in range(workers)]
     sums = [0.0] * workers
     classes: list[list[str]] = [[] for _ in range(workers)]
+    messages: list[str] = []
 
     def worker(r):
         eng = model = None
         try:
-            eng = api.Engine(engine_threads, r, sink, r % ndev)
+            eng = api.Engine(engine_threads, r, sink, device)
             model = api.SynthModel(eng, transport, r, workers, list(sizes), mode=mode,
                                    bucket_bytes=bucket_bytes, outstanding=outstanding if mode == "concom" else 1,
                                    lr=0.1, rescale=1.0 / global_batch, momentum=momentum,
@@ -160,6 +162,7 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
             sums[r] = model.checksum()
         except CsError as e:
             classes[r].append(e.kind)
+            messages.append(f"rank {r}: {e}")
             transport.abort()  # fail_slot analogue: release the other ranks (collective.cpp:92-105)
         finally:
             try:
@@ -190,7 +193,8 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
     m.error = primary_error(m.error_classes)
     gauge_max, overlap = sink.gauges()
     m.max_concurrent_collectives, m.compute_overlap_observed = gauge_max, overlap
-    m.b200 = {"path": "local transport rank threads, kernel (b) rank-order sums", "devices": ndev,
+    m.b200 = {"path": "local transport rank threads, kernel (b) rank-order sums", "device": device,
+              "error_messages": messages,
               "keys": len(sizes), "params": int(sum(sizes)), "steps_per_epoch": steps_per_epoch,
               "bucket_bytes": bucket_bytes, "weight_checksums": sums,
               "final_train_loss": "n/a (synthetic backward: no loss)"}

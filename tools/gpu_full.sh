@@ -6,3 +6,8 @@ for N in ${NS:-2 4}; do
 timeout 600 python -m torch.distributed.run --nproc-per-node $N --master-addr 127.0.0.1 --master-port $((29950+N)) bench.py --gpus $N > gpurun_out/full_bench_n$N.log 2>&1
 done
 timeout 600 python bench.py --impl reference > gpurun_out/full_ref_n1.log 2>&1
+# real ResNet-50 through the KvStore (replicated / ZeRO-1) vs DDP at N=4
+port=29990
+for opt in "--impl kv" "--impl kv --zero" "--impl ddp" "--impl local"; do port=$((port+1))
+timeout 600 python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $port tools/train_resnet50.py $opt 2>/dev/null | grep '^{' >> gpurun_out/full_train4.txt
+done
