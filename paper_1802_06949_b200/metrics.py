@@ -120,7 +120,8 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
                   epochs: int = 2, steps_per_epoch: int = 3, sizes: Sequence[int] = (4096,) * 8,
                   bucket_bytes: int = 0, seed: int = 1, global_batch: int = 64, momentum: float = 0.0,
                   backward_ms: float = 0.0, watchdog_ms: int = 30000, model_name: str = "synthetic",
-                  trace_path: str | None = None, metrics_path: str | None = None, device: int = 0) -> Metrics:
+                  trace_path: str | None = None, metrics_path: str | None = None, device: int = 0,
+                  inject_latency_us: int = 0) -> Metrics:
     """runner.cpp:47-135 over the GPU path: validate, one transport + trace
     sink, communicators for ConCom, rank threads each running the native
     trainer loop shape, then the metrics (epoch wall time averaged over
@@ -138,8 +139,11 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
         raise ConfigError(-1, "run: global batch size must divide evenly across workers")
     if mode == "concom" and outstanding < 1:
         raise ConfigError(-1, "run: concom requires outstanding >= 1")
+    if inject_latency_us < 0:
+        raise ConfigError(-1, "run: injected latency must be >= 0")
     sink = api.TraceSink()
     transport = api.Transport.local(workers, watchdog_ms, sink)
+    transport.set_inject_latency(inject_latency_us)
     comms = api.create_communicators(transport, outstanding) if mode == "concom" else []
     walls = [[] for _ in range(workers)]
     sums = [0.0] * workers
