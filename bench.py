@@ -176,7 +176,7 @@ def peaks() -> dict:
 
 # ------------------------------------------------------------- reference
 
-def run_reference(args, keys, mode, outstanding, world):
+def run_reference(args, keys, mode, outstanding, world, warmup=1, iters=None):
     """The reference's own CPU path (Engine + KvStore + Transport, compiled
     from /root/reference into oracle/_ref) on the host cores."""
     sys.path.insert(0, str(ROOT / "tests"))
@@ -191,7 +191,8 @@ def run_reference(args, keys, mode, outstanding, world):
     threads = max(2, ncores // ranks)
     sizes = (C.c_int64 * len(keys))(*keys)
     stats = (C.c_double * 2)()
-    rc = R.ref_bench(mode.encode(), ranks, threads, outstanding, len(keys), sizes, 1, args.cpu_steps, 0,
+    iters = args.cpu_steps if iters is None else iters
+    rc = R.ref_bench(mode.encode(), ranks, threads, outstanding, len(keys), sizes, warmup, iters, 0,
                      0.1, 1.0 / (64 * ranks), stats)
     if rc != 0:
         raise RuntimeError(R.ref_last_error().decode())
@@ -206,19 +207,23 @@ def reference_main(args, cfg_name, keys, mode, outstanding, config):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    ref = run_reference(args, keys, mode, outstanding, world)
+    # the driver's --steps / --warmup, bounded so the arm stays within a few
+    # minutes on the host cores (one fp64 ResNet-50 step is ~0.1-2 s)
+    warmup, steps = max(1, min(args.warmup, 3)), max(1, min(args.steps, 10))
+    ref = run_reference(args, keys, mode, outstanding, world, warmup, steps)
     if ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcollsim_ref.so not built"}))
         return
     line = {
         "metric": METRIC, "impl": "reference", "value": round(ref["value"], 4), "unit": "GB/s",
-        "n_gpus": world, "steps": args.cpu_steps, "warmup": 1, "ms_per_step": round(ref["ms_per_step"], 3),
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": round(ref["ms_per_step"], 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (random_uniform seeds 1000+r*K+k)", "config": config,
         "cpu_baseline": {"value": round(ref["value"], 4), "unit": "GB/s", "cores": ref["cores"],
                          "kind": "reference",
                          "sample": f"{len(keys)} keys, {ref['ranks']} rank threads x {ref['threads']} engine "
-                                   f"threads, fp64, {args.cpu_steps} iterations after 1 warm-up"},
+                                   f"threads, fp64, {steps} iterations after {warmup} warm-up "
+                                   f"(--steps/--warmup capped at 10/3 for the CPU arm)"},
         "e2e": {"value": round(ref["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

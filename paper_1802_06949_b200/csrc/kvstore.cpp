@@ -90,6 +90,13 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
     for (int i = 0; i < cfg_.outstanding; ++i) comm_lanes_.push_back(engine_.new_lane(cfg_.comm_priority));
   pack_lane_ = engine_.new_lane(cfg_.comm_priority);
   update_lane_ = engine_.new_lane(0);
+  // CSB_KV_LANES=1: packs, world collectives and updates share one stream
+  // (no cross-stream event hops; buckets then no longer overlap each other)
+  static const bool one_lane = [] {
+    const char* e = std::getenv("CSB_KV_LANES");
+    return e && std::string(e) == "1";
+  }();
+  if (one_lane && cfg_.mode != KvMode::ConCom) pack_lane_ = update_lane_ = world_lane_;
 }
 
 KvStore::~KvStore() {

@@ -141,6 +141,34 @@ def main():
             res[f"w{so}"], res[f"m{so}"], res[f"buf{so}"] = w.cpu().numpy(), m.cpu().numpy(), buf.cpu().numpy()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)
         eng.close()
+    elif case == "zero_vs_replicated":
+        # the same fp32 weights / bf16 comm / momentum run through the fused
+        # kernel with a replicated update and with ZeRO-1: identical weights
+        sizes = [1, 7, 64, 300, 4097, 70000, 1 << 18]
+        K = len(sizes)
+        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)  # noqa: E731
+        res = {}
+        for zero in (0, 1):
+            for cdt in (api.F32, api.BF16):
+                eng = Engine(4, rank, None, local)
+                store = KvStore(eng, tr, rank, KvConfig("depcha", 1, K, comm_dtype=cdt, bucket_bytes=256 * 1024,
+                                                        issue_order=1, p2p=1, zero=zero))
+                ws = [Slot(f32(O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n)),
+                           eng.new_variable()) for k, n in enumerate(sizes)]
+                gs = [Slot(f32(O.random_uniform(n, 1000 + rank * K + k)), eng.new_variable())
+                      for k, n in enumerate(sizes)]
+                for k in range(K):
+                    store.init(k, ws[k])
+                eng.wait_all()
+                for _ in range(3):
+                    store.push(list(range(K)), gs)
+                    store.pull_update(list(range(K)), ws, 0.1, 1.0 / 64, 0.9)
+                eng.wait_all()
+                for k in range(K):
+                    res[f"z{zero}_c{cdt}_k{k}"] = ws[k].value.cpu().numpy()
+                store.close()
+                eng.close()
+        np.savez(outdir / f"{case}_r{rank}.npz", **res)
     elif case in ("torch_dp", "torch_dp_zero"):
         # real-backward producer over the fused NVLink kernel: save every
         # rank's per-step gradients and weights; the test replays the oracle

@@ -182,6 +182,23 @@ def test_torch_producer_over_nvlink_bit_exact(two_gpus, tmp_path, case):
                 np.testing.assert_array_equal(outs[r][f"w{step + 1}"], w, err_msg=f"R={R} rank {r} step {step}")
 
 
+def test_zero_equals_replicated_update_fp32_and_bf16(two_gpus, tmp_path):
+    """ZeRO-1 (sharded master weights + momentum, weight all-gather) gives
+    bit-identical weights to the replicated fused update, with fp32 and with
+    bf16 comm buckets (the kernel reproduces the bucket's bf16 rounding of
+    the sum), momentum 0.9, 3 steps, keys straddling shard boundaries."""
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("zero_vs_replicated", R, d)
+        outs = [np.load(d / f"zero_vs_replicated_r{r}.npz") for r in range(R)]
+        for r in range(R):
+            for name in outs[r].files:
+                if name.startswith("z1_"):
+                    np.testing.assert_array_equal(outs[r][name], outs[r]["z0_" + name[3:]], err_msg=f"R={R} {name}")
+                np.testing.assert_array_equal(outs[r][name], outs[0][name])
+
+
 def test_nvls_fused_allreduce_update_within_tolerance(two_gpus, tmp_path):
     """fp32 DepCha through the NVSwitch multicast path (multimem.ld_reduce /
     multimem.st) fused with the momentum update: within the north-star fp32
