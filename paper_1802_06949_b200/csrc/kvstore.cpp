@@ -105,6 +105,7 @@ KvStore::~KvStore() {
   } catch (...) {
   }
   engine_.bind_device();
+  for (const auto& peers : shared_) transport_.unshare_buffer(peers);
   for (KeyState& k : keys_)
     if (k.mom) cudaFree(k.mom);
   for (void* p : allocations_) cudaFree(p);
@@ -300,6 +301,7 @@ void KvStore::build_buckets() {
   } else if (p2p_active_) {
     // setup-phase collective: every rank maps every peer's arena (CUDA IPC)
     const std::vector<void*> peers = transport_.share_buffer(arena);
+    shared_.push_back(peers);
     for (Bucket& b : bs) {
       const uint64_t boff = static_cast<uint64_t>(static_cast<char*>(b.base) - arena);
       for (void* p : peers) b.peer_bufs.push_back(static_cast<char*>(p) + boff);
@@ -320,6 +322,7 @@ void KvStore::build_buckets() {
     allocations_.push_back(master);
     allocations_.push_back(mom);
     const std::vector<void*> peers = transport_.share_buffer(master);
+    shared_.push_back(peers);
     uint64_t soff = 0;
     for (Bucket& b : bs) {
       for (void* p : peers) b.wm_peers.push_back(static_cast<char*>(p) + soff * ws);

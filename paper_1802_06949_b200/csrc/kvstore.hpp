@@ -182,6 +182,7 @@ class KvStore {
   void* arena_ = nullptr;
   uint64_t arena_bytes_ = 0;
   bool zero_active_ = false;  // ZeRO-1 (cfg_.zero over an active peer-memory path)
+  std::vector<std::vector<void*>> shared_;  // share_buffer results, unmapped at destruction
   int zero_wdt_ = -1;
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call
   uint32_t stamp_ = 0;

@@ -1,6 +1,8 @@
 // transport.cpp -- see transport.hpp.
 #include "transport.hpp"
 
+#include <algorithm>
+
 #include "hostprof.hpp"
 #include "kernels.hpp"
 
@@ -171,6 +173,18 @@ std::vector<void*> Transport::share_buffer(void* base) {
     ptrs[r] = p;
   }
   return ptrs;
+}
+
+void Transport::unshare_buffer(const std::vector<void*>& ptrs) {
+  std::lock_guard<std::mutex> lock(mu_);
+  cudaSetDevice(device_);
+  for (size_t r = 0; r < ptrs.size(); ++r) {
+    if (static_cast<int>(r) == rank_ || !ptrs[r]) continue;
+    auto it = std::find(ipc_opened_.begin(), ipc_opened_.end(), ptrs[r]);
+    if (it == ipc_opened_.end()) continue;
+    cudaIpcCloseMemHandle(*it);
+    ipc_opened_.erase(it);
+  }
 }
 
 NvlsBuffer Transport::alloc_nvls(size_t bytes) {

@@ -73,6 +73,10 @@ class Transport {
   // allocation, in the same order; returns every rank's mapping of its peer
   // (CUDA IPC handles exchanged through the ledger), own entry = base.
   std::vector<void*> share_buffer(void* base);
+  // Closes this rank's mappings of the peers' buffers returned by
+  // share_buffer (before the owner of `ptrs` frees its own buffer, so the
+  // same addresses can be shared again later).
+  void unshare_buffer(const std::vector<void*>& ptrs);
   struct P2PUpdate {
     const DeviceTable::Entry* tab = nullptr;  // bucket-group coordinates, sorted
     int n_entries = 0;
