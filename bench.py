@@ -246,6 +246,7 @@ def main():
               "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
               "issue_order": args.issue_order, "momentum": args.momentum, "parallelism": f"dp{world}",
               "l2": "inputs larger than L2 (no flush)",
+              "producer_order": "per-rank random (seeded)" if args.config == "stress" else "reverse key order",
               "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
               else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"}
     if args.impl == "reference":
@@ -289,7 +290,8 @@ def main():
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
                   p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
-                  zero=args.zero and args.comm == "p2p")
+                  zero=args.zero and args.comm == "p2p",
+                  order_seed=1 if args.config == "stress" else 0)
     config["collectives"] = ("identity (1 rank)" if world == 1 else
                              {"nccl": "NCCL",
                               "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",

@@ -275,6 +275,8 @@ typedef struct cs_synth_config {
   int p2p;                /* as cs_kv_config.p2p */
   int grad_views;         /* 1: gradients are produced in place in the comm buckets (cs_kv_bucket_view) */
   int zero;               /* as cs_kv_config.zero */
+  int order_seed;         /* != 0: this rank's gradients become ready in a random order (seeded per
+                             rank) -- the deadlock-stress producer of SURVEY §8d config 5 */
 } cs_synth_config;
 enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,

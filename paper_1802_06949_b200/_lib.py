@@ -147,7 +147,7 @@ class SynthConfigC(C.Structure):
                 ("lr", C.c_double), ("rescale", C.c_double), ("momentum", C.c_double),
                 ("backward_ns", C.c_uint64), ("backward_ctas", C.c_int), ("fused_update", C.c_int),
                 ("comm_priority", C.c_int), ("host_source", C.c_int), ("p2p", C.c_int),
-                ("grad_views", C.c_int), ("zero", C.c_int)]
+                ("grad_views", C.c_int), ("zero", C.c_int), ("order_seed", C.c_int)]
 
 
 CS_STEP_BACKWARD, CS_STEP_COMM, CS_STEP_LOCAL_UPDATE, CS_STEP_CHECKSUM = 1, 2, 4, 8

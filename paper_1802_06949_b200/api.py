@@ -581,11 +581,12 @@ class SynthModel:
                  rescale: float = 1.0, momentum: float = 0.0, backward_ns: int = 0,
                  backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0, p2p: bool = False,
                  host_source: bool = False, concom_comms: Sequence[int] = (),
-                 ready_ms: Sequence[float] | None = None, grad_views: bool = False, zero: bool = False):
+                 ready_ms: Sequence[float] | None = None, grad_views: bool = False, zero: bool = False,
+                 order_seed: int = 0):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
                                 int(fused_update), comm_priority, int(host_source), int(p2p), int(grad_views),
-                                int(zero))
+                                int(zero), int(order_seed))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()

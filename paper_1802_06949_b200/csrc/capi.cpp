@@ -612,6 +612,7 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     c.p2p = cfg->p2p;
     c.grad_views = cfg->grad_views != 0;
     c.zero = cfg->zero;
+    c.order_seed = cfg->order_seed;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
@@ -648,6 +649,7 @@ int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nran
     c.p2p = cfg->p2p;
     c.grad_views = cfg->grad_views != 0;
     c.zero = cfg->zero;
+    c.order_seed = cfg->order_seed;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);

@@ -160,6 +160,12 @@ void SynthModel::init() {
       prev = std::max(prev, cfg_.ready_ms[k]);
     }
   } else {
+    if (cfg_.order_seed != 0) {
+      // deadlock stress: every rank produces its gradients in its own random
+      // order (the schedules must still issue identical collective sequences)
+      std::mt19937_64 g(mix_seed(static_cast<uint64_t>(cfg_.order_seed), static_cast<uint64_t>(rank_)));
+      std::shuffle(produce_order_.begin(), produce_order_.end(), g);
+    }
     for (int k = 0; k < K; ++k)
       spin_ns_[k] = cfg_.backward_ns == 0
                         ? 0

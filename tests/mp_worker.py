@@ -141,6 +141,24 @@ def main():
             res[f"w{so}"], res[f"m{so}"], res[f"buf{so}"] = w.cpu().numpy(), m.cpu().numpy(), buf.cpu().numpy()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)
         eng.close()
+    elif case == "stress_order":
+        # deadlock stress (scaled): every rank produces
+        # its gradients in its own random order; the schedules must still
+        # issue one collective sequence, and the weights cannot depend on it
+        from paper_1802_06949_b200 import keysets
+        sizes = [min(n, 1 << 16) for n in keysets.stress_keys(96)]
+        out["sums"] = {}
+        for mode, p2p, zero in (("depcha", 1, 1), ("depcha", 1, 0), ("funnel", 1, 0), ("depcha", 0, 0)):
+            for seed in (0, 11):
+                eng = Engine(4, rank, None, local)
+                m = api.SynthModel(eng, tr, rank, world, sizes, mode=mode, bucket_bytes=(256 * 1024 if p2p else 0),
+                                   issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=0.9, backward_ns=int(2e6),
+                                   p2p=p2p, zero=bool(zero), order_seed=seed)
+                m.init()
+                m.run(3, m.BACKWARD | m.COMM)
+                out["sums"][f"{mode}_p{p2p}_z{zero}_s{seed}"] = m.checksum()
+                m.close()
+                eng.close()
     elif case == "zero_vs_replicated":
         # the same fp32 weights / bf16 comm / momentum run through the fused
         # kernel with a replicated update and with ZeRO-1: identical weights
