@@ -254,7 +254,7 @@ def main():
     if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
         args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
     config["optimizer_state"] = ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
-                                 "fused kernel" if (args.zero and args.comm == "p2p" and world > 1)
+                                 "fused kernel" if (args.zero and args.comm == "p2p" and mode == "depcha" and world > 1)
                                  else "replicated on every rank")
 
     import torch
@@ -284,13 +284,17 @@ def main():
     transport = api.Transport.nccl(name[0], world, rank, local_rank, 120000)
     comms_main = api.create_communicators(transport, outstanding) if mode == "concom" else []
     comms_e2e = api.create_communicators(transport, outstanding) if (mode == "concom" and not args.no_extras) else []
+    # communicators for the schedule comparison (setup-only, before any collective)
+    sched_outstanding = 4
+    comms_sched = (api.create_communicators(transport, sched_outstanding)
+                   if (world > 1 and not args.no_extras and mode != "concom") else [])
     engine = api.Engine(args.engine_threads, rank, None, local_rank)
     common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
                   p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
-                  zero=args.zero and args.comm == "p2p",
+                  zero=args.zero and args.comm == "p2p" and mode == "depcha",
                   order_seed=1 if args.config == "stress" else 0)
     config["collectives"] = ("identity (1 rank)" if world == 1 else
                              {"nccl": "NCCL",
@@ -374,7 +378,7 @@ def main():
             # peer loads: (N-1)/N of the gradients in the reduce-scatter, plus
             # (N-1)/N of the reduced gradients (replicated update) or of the
             # fp32 master weights (ZeRO-1 all-gather); NVLS: 1 x bucket bytes
-            zero_on = args.zero and args.comm == "p2p"
+            zero_on = args.zero and args.comm == "p2p" and mode == "depcha"
             second = sum(keys) * 4 if zero_on else gbytes
             link_step = ((world - 1) / world * (gbytes + second) if args.comm == "p2p" else gbytes)
             bytes_launch = link_step * n_prof / max(1, ks["launches"])
@@ -397,6 +401,34 @@ def main():
                                             "ms_per_step": round(v["total_ms"] / max(3, min(args.steps, 10)), 4),
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}
                                         for k, v in kstats.items()}}
+
+        # ---- the paper's three schedules on the same gradient set (N>1)
+        if world > 1:
+            scheds = {mode: {"value": line["value"], "ms_per_step": line["ms_per_step"],
+                             "collectives": config["collectives"]}}
+            for sched in ("funnel", "depcha", "concom"):
+                if sched in scheds:
+                    continue
+                if sched == "concom":
+                    if not comms_sched:
+                        continue
+                    kw = {**common, "mode": "concom", "outstanding": sched_outstanding, "p2p": 0, "zero": False,
+                          "bucket_bytes": 25 << 20}
+                    coll = f"NCCL, {sched_outstanding} communicators, 25 MiB buckets"
+                    cc = comms_sched
+                else:
+                    kw = {**common, "mode": sched, "zero": common["zero"] and sched == "depcha"}
+                    coll = config["collectives"]
+                    cc = []
+                ms_s = api.SynthModel(engine, transport, rank, world, keys, concom_comms=cc, **kw)
+                ms_s.init()
+                ms_s.run(args.warmup, COMM)
+                barrier()
+                t_s = max_over_ranks(ms_s.run(args.steps, COMM)) / args.steps
+                scheds[sched] = {"value": round(world * gbytes / (t_s * 1e6), 3), "ms_per_step": round(t_s, 4),
+                                 "collectives": coll}
+                ms_s.close()
+            line["schedules"] = scheds
 
         # ---- the same aggregation with gradient-as-bucket-view (no pack copy)
         if not args.grad_views and bucket_mb > 0:

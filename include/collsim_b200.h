@@ -213,7 +213,7 @@ typedef struct cs_kv_config {
   int p2p;               /* 1: NVLink peer-memory collectives (needs bucket_bytes > 0 and a
                             peer-capable NCCL transport); DepCha pull_update becomes one fused
                             allreduce+update kernel per bucket, rank-order (bit-exact) sums */
-  int zero;              /* 1 (with p2p = 1): ZeRO-1 -- each rank keeps master weights and momentum of
+  int zero;              /* 1 (DepCha, p2p = 1): ZeRO-1 -- each rank keeps master weights and momentum of
                             its shard only; the fused kernel reduce-scatters, updates the shard and
                             all-gathers the weights.  pull_update must cover whole buckets. */
 } cs_kv_config;

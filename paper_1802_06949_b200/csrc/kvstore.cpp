@@ -72,8 +72,10 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   // hold the SMs the other needs on a peer, so ConCom stays on NCCL.
   if (cfg_.p2p && cfg_.mode == KvMode::ConCom)
     throw ConfigError("KvStore: the peer-memory path runs on one ordered comm stream (funnel/depcha)");
-  if (cfg_.zero && (cfg_.p2p != 1 || cfg_.mode == KvMode::ConCom || cfg_.mode == KvMode::Naive))
-    throw ConfigError("KvStore: ZeRO-1 runs on the peer-memory path (p2p = 1) under funnel/depcha");
+  // ZeRO-1 lives in DepCha's fused pull (Funnel/ConCom issue the collective
+  // at push, before the weights are known)
+  if (cfg_.zero && (cfg_.p2p != 1 || cfg_.mode != KvMode::DepCha))
+    throw ConfigError("KvStore: ZeRO-1 runs on the peer-memory path (p2p = 1) under depcha");
   // one rank: nothing crosses NVLink, the collectives are the identity
   p2p_active_ = cfg_.p2p != 0 && transport_.p2p_capable();
   zero_active_ = p2p_active_ && cfg_.zero;

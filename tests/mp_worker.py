@@ -148,7 +148,7 @@ def main():
         from paper_1802_06949_b200 import keysets
         sizes = [min(n, 1 << 16) for n in keysets.stress_keys(96)]
         out["sums"] = {}
-        for mode, p2p, zero in (("depcha", 1, 1), ("depcha", 1, 0), ("funnel", 1, 0), ("depcha", 0, 0)):
+        for mode, p2p, zero in (("depcha", 1, 1), ("depcha", 1, 0), ("funnel", 1, 0), ("depcha", 0, 0)):  # noqa
             for seed in (0, 11):
                 eng = Engine(4, rank, None, local)
                 m = api.SynthModel(eng, tr, rank, world, sizes, mode=mode, bucket_bytes=(256 * 1024 if p2p else 0),
