@@ -559,6 +559,7 @@ struct P2PParams {
   uint64_t groups, slot_groups;
   double step, mu;
   int nranks, rank, n_entries, shard_only;
+  int sys_fence;  // explicit fence.sc.sys before the release store of a pair barrier (CSB_P2P_FENCE)
   uint32_t epoch;
 };
 
@@ -577,7 +578,10 @@ __device__ __forceinline__ void pair_barrier(const P2PParams& p, int phase) {
   __syncthreads();
   const int t = threadIdx.x;
   if (t < p.nranks) {
-    __threadfence_system();
+    // the release store publishes what this CTA wrote before the __syncthreads
+    // (barrier + release, as CUTLASS's arrive); CSB_P2P_FENCE=1 adds a
+    // fence.sc.sys in front (measured ~10 % slower on 25 MiB buckets)
+    if (p.sys_fence) __threadfence_system();
     const size_t slot = (static_cast<size_t>(phase) * CS_MAX_RANKS + p.rank) * kP2PMaxCtas + blockIdx.x;
     flag_store(p.flags[t] + slot, p.epoch);
     const uint32_t* mine =
@@ -1609,7 +1613,19 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
 #undef CSB_ZERO_PICK
   }
   if (!fn) throw UsageError("p2p_allreduce: unsupported dtype combination");
-  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
+  // cooperative launch: the driver guarantees every CTA is resident (the
+  // pair barriers need it); CSB_P2P_COOP=0 measured no faster
+  static const bool coop = [] {
+    const char* e = std::getenv("CSB_P2P_COOP");
+    return !(e && std::string(e) == "0");
+  }();
+  static const int fence = [] {
+    const char* e = std::getenv("CSB_P2P_FENCE");
+    return (e && std::string(e) == "1") ? 1 : 0;
+  }();
+  p.sys_fence = fence;
+  if (coop) CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
+  else CSB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   ls.done();
 }
 
