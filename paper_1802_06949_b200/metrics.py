@@ -121,7 +121,7 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
                   bucket_bytes: int = 0, seed: int = 1, global_batch: int = 64, momentum: float = 0.0,
                   backward_ms: float = 0.0, watchdog_ms: int = 30000, model_name: str = "synthetic",
                   trace_path: str | None = None, metrics_path: str | None = None, device: int = 0,
-                  inject_latency_us: int = 0) -> Metrics:
+                  inject_latency_us: int = 0, lr: float = 0.1) -> Metrics:
     """runner.cpp:47-135 over the GPU path: validate, one transport + trace
     sink, communicators for ConCom, rank threads each running the native
     trainer loop shape, then the metrics (epoch wall time averaged over
@@ -156,7 +156,7 @@ def run_synthetic(mode: str = "depcha", workers: int = 2, engine_threads: int = 
             eng = api.Engine(engine_threads, r, sink, device)
             model = api.SynthModel(eng, transport, r, workers, list(sizes), mode=mode,
                                    bucket_bytes=bucket_bytes, outstanding=outstanding if mode == "concom" else 1,
-                                   lr=0.1, rescale=1.0 / global_batch, momentum=momentum,
+                                   lr=lr, rescale=1.0 / global_batch, momentum=momentum,
                                    backward_ns=int(backward_ms * 1e6), concom_comms=comms)
             model.init()
             for _ in range(epochs):

@@ -112,3 +112,22 @@ def test_failed_run_reports_primary_error(gpu):
     from paper_1802_06949_b200 import ConfigError
     with pytest.raises(ConfigError, match="outstanding"):
         run_synthetic(mode="concom", outstanding=0)
+
+
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+def test_cli_run_emits_reference_metrics(gpu, tmp_path, mode):
+    """`python -m paper_1802_06949_b200 run` (the collsim CLI drop-in): exit 0,
+    collsim-metrics-v1 on stdout equal to the --metrics file, a trace file."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    mpath, tpath = tmp_path / "m.json", tmp_path / "t.jsonl"
+    r = subprocess.run([sys.executable, "-m", "paper_1802_06949_b200", "run", "--mode", mode, "--workers", "2",
+                        "--epochs", "2", "--model", "diamond", "--samples", "256", "--metrics", str(mpath),
+                        "--trace", str(tpath)], capture_output=True, text=True, cwd=root, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    m = metrics_from_json(r.stdout)
+    assert m.ok() and m.mode == mode and m.model == "diamond" and len(m.epoch_times_s) == 2
+    assert metrics_from_json(mpath.read_text()) == m
+    assert tpath.stat().st_size > 0
