@@ -81,3 +81,26 @@ def test_kernels_reject_bad_arguments_without_a_gpu():
 def test_device_count_is_zero_here_or_positive_on_box():
     from paper_1802_06949_b200 import device_count
     assert device_count() >= 0
+
+
+def test_kvstore_config_validation_before_any_device_work():
+    """kvstore.cpp:41-51 checks plus the B200 options: every inconsistent
+    configuration is a ConfigError raised by the constructor, on any host."""
+    from paper_1802_06949_b200 import ConfigError, Engine, KvConfig, KvStore, Transport
+    eng = Engine(1, 0, None, -1)  # host-only engine
+    tr = Transport.ledger_only(2)
+    bad = [
+        (KvConfig("funnel", 1, 0), "num_keys"),
+        (KvConfig("concom", 0, 4), "outstanding"),
+        (KvConfig("depcha", 1, 4, p2p=1), "fusion buckets"),
+        (KvConfig("concom", 1, 4, bucket_bytes=1 << 20, p2p=1), "one ordered comm stream"),
+        (KvConfig("funnel", 1, 4, bucket_bytes=1 << 20, p2p=1, zero=1), "ZeRO-1"),
+        (KvConfig("depcha", 1, 4, bucket_bytes=1 << 20, zero=1), "ZeRO-1"),
+    ]
+    for cfg, msg in bad:
+        with pytest.raises(ConfigError, match=msg):
+            KvStore(eng, tr, 0, cfg, [1] * cfg.outstanding if cfg.mode == "concom" else [])
+    with pytest.raises(ConfigError, match="CUDA device"):  # a valid config still needs a device engine
+        KvStore(eng, tr, 0, KvConfig("depcha", 1, 4))
+    eng.close()
+    tr.close()
