@@ -46,8 +46,8 @@ CONFIGS = {
     # name: (keyset, mode, outstanding, dtype, bucket_mb, backward calibration or fixed ms)
     "resnet50": ("resnet50", "depcha", 1, "fp32", 100, "resnet50_b64.json"),
     "alexnet": ("alexnet", "concom", 4, "fp32", 25, "alexnet_b64_amp.json"),
-    "resnet152": ("resnet152", "depcha", 1, "bf16", 25, "resnet152_b64_amp.json"),
-    "inception_v3": ("inception_v3", "depcha", 1, "bf16", 25, 30.0),
+    "resnet152": ("resnet152", "depcha", 1, "bf16", 128, "resnet152_b64_amp.json"),
+    "inception_v3": ("inception_v3", "depcha", 1, "bf16", 128, 30.0),
     "stress": ("stress", "depcha", 1, "fp32", 64, 0.0),
     "uniform16": ("uniform16x1048576", "funnel", 1, "fp32", 0, 0.0),
 }
@@ -84,8 +84,10 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-zero", dest="zero", action="store_false",
-                   help="replicated optimizer state instead of ZeRO-1 (the fused kernel's default at N>1: "
-                        "sharded master weights + momentum, weight all-gather, bit-identical results)")
+                   help="replicated optimizer state instead of ZeRO-1 (the fused kernel's default at N>1 for "
+                        "fp32 gradients: sharded master weights + momentum, weight all-gather, bit-identical "
+                        "results; bf16 gradient sets keep the replicated update, whose all-gather moves bf16 "
+                        "sums instead of fp32 weights)")
     p.add_argument("--grad-views", action="store_true",
                    help="gradients produced in place in the comm buckets (gradient-as-bucket-view): "
                         "push copies nothing")
@@ -254,7 +256,7 @@ def main():
     if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
         args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
     config["optimizer_state"] = ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
-                                 "fused kernel" if (args.zero and args.comm == "p2p" and mode == "depcha" and world > 1)
+                                 "fused kernel" if (args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32" and world > 1)
                                  else "replicated on every rank")
 
     import torch
@@ -294,7 +296,7 @@ def main():
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
                   p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
-                  zero=args.zero and args.comm == "p2p" and mode == "depcha",
+                  zero=args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32",
                   order_seed=1 if args.config == "stress" else 0)
     config["collectives"] = ("identity (1 rank)" if world == 1 else
                              {"nccl": "NCCL",
@@ -384,7 +386,7 @@ def main():
             # peer loads: (N-1)/N of the gradients in the reduce-scatter, plus
             # (N-1)/N of the reduced gradients (replicated update) or of the
             # fp32 master weights (ZeRO-1 all-gather); NVLS: 1 x bucket bytes
-            zero_on = args.zero and args.comm == "p2p" and mode == "depcha"
+            zero_on = args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32"
             second = sum(keys) * 4 if zero_on else gbytes
             link_step = ((world - 1) / world * (gbytes + second) if args.comm == "p2p" else gbytes)
             bytes_launch = link_step * n_prof / max(1, ks["launches"])
