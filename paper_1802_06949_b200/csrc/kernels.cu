@@ -547,6 +547,14 @@ constexpr int kP2PMaxCtas = 1184;
 // on all 512.
 constexpr int kP2PThreads = 512;
 constexpr int kP2PLinkThreads = 256;
+// Threads issuing the peer loads of a reduce phase.  With 2 ranks each
+// thread has only one remote 16-B load in flight, so the whole CTA takes
+// part (tools/nvlink_probe.cu at 2 GPUs: 266 GB/s with 256 threads/SM,
+// 532 with 1024); from 3 ranks on, 256 threads keep enough in flight.
+template <int M>
+constexpr int reduce_threads() {
+  return M == 2 ? kP2PThreads : kP2PLinkThreads;
+}
 
 struct P2PParams {
   void* bufs[CS_MAX_RANKS];
@@ -601,8 +609,9 @@ template <int CDT, int M>
 __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
   using Acc = typename AccOf<CDT, CDT>::T;
   const int m = (M > 0) ? M : p.nranks;
-  if (threadIdx.x >= kP2PLinkThreads) return;
-  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+  constexpr int NT = reduce_threads<M>();
+  if (threadIdx.x >= NT) return;
+  for (uint64_t q = a + threadIdx.x; q < b; q += NT) {
     const uint64_t i = q * kVec;
     Acc acc[kVec];
     if constexpr (M > 0) {
@@ -849,9 +858,10 @@ __device__ __forceinline__ void zero_reduce_update(const P2PParams& p, uint64_t 
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
   const WAcc step = static_cast<WAcc>(p.step), mu = static_cast<WAcc>(p.mu);
   const int m = (M > 0) ? M : p.nranks;
-  if (threadIdx.x >= kP2PLinkThreads) return;
+  constexpr int NT = reduce_threads<M>();
+  if (threadIdx.x >= NT) return;
   void* wm = p.wm[p.rank];
-  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
+  for (uint64_t q = a + threadIdx.x; q < b; q += NT) {
     const uint64_t i = q * kVec, j = (q - s0) * kVec;  // bucket element / shard-local element
     CAcc acc[kVec];
     if constexpr (M > 0) {
