@@ -560,11 +560,10 @@ struct P2PParams {
   void* bufs[CS_MAX_RANKS];
   uint32_t* flags[CS_MAX_RANKS];
   void* mc;  // NVLS: multicast VA of the bucket (bufs unused in phase 1)
-  void* recv[CS_MAX_RANKS];  // push mode: every rank's receive area (nranks slots of slot_groups)
   void* wm[CS_MAX_RANKS];    // ZeRO-1: every rank's master-weight shard (shard-local layout)
   void* mom_b;               // ZeRO-1: this rank's momentum shard (shard-local layout)
   const DevEntry* tab;
-  uint64_t groups, slot_groups;
+  uint64_t groups;
   double step, mu;
   int nranks, rank, n_entries, shard_only;
   int sys_fence;  // explicit fence.sc.sys before the release store of a pair barrier (CSB_P2P_FENCE)
@@ -694,83 +693,6 @@ __device__ __forceinline__ void nvls_reduce_chunk(const P2PParams& p, uint64_t a
   }
 }
 
-// Push mode, phase 0: CTA c copies chunk c of every peer's shard out of the
-// local bucket into slot `rank` of that peer's receive area -- NVLink carries
-// only posted writes (no remote-read round trips).  Destinations are staggered
-// (rank+1, rank+2, ...) so the N senders spread over the N receivers.
-template <int CDT>
-__device__ __forceinline__ void p2p_push_chunks(const P2PParams& p) {
-  constexpr uint64_t kGroupBytes = kVec * (CDT == CS_F64 ? 8 : CDT == CS_F32 ? 4 : 2);
-  const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
-  for (int k = 1; k < p.nranks; ++k) {
-    const int s = (p.rank + k) % p.nranks;
-    const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
-    const uint64_t a = s0 + L * c / G, b = s0 + L * (c + 1) / G;
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(p.bufs[p.rank]) + a * kGroupBytes);
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(p.recv[s]) +
-                                          (static_cast<uint64_t>(p.rank) * p.slot_groups + (a - s0)) * kGroupBytes);
-    const uint64_t n = (b - a) * (kGroupBytes / 16);
-    uint64_t i = threadIdx.x;
-    if (i >= kP2PLinkThreads) return;
-    for (; i + 3 * kP2PLinkThreads < n; i += 4 * kP2PLinkThreads) {
-      uint4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = src[i + u * kP2PLinkThreads];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dst[i + u * kP2PLinkThreads] = v[u];
-    }
-    for (; i < n; i += kP2PLinkThreads) dst[i] = src[i];
-  }
-}
-
-// Push mode, phase 1: every addend of my shard chunk is now local (slot r of
-// my receive area, or my own bucket for r == rank); sum in rank order and
-// write the result into every rank's bucket.
-template <int CDT, int M>
-__device__ __forceinline__ void p2p_push_reduce_chunk(const P2PParams& p, uint64_t s0, uint64_t a, uint64_t b) {
-  using Acc = typename AccOf<CDT, CDT>::T;
-  const int m = (M > 0) ? M : p.nranks;
-  if (threadIdx.x >= kP2PLinkThreads) return;
-  for (uint64_t q = a + threadIdx.x; q < b; q += kP2PLinkThreads) {
-    const uint64_t i = q * kVec;
-    const uint64_t j = (q - s0) * kVec;
-    Acc acc[kVec];
-    if constexpr (M > 0) {
-      Acc x[M][kVec];
-#pragma unroll
-      for (int r = 0; r < M; ++r) {
-        const bool own = (r == p.rank);
-        load8<CDT, Acc>(own ? p.bufs[r] : p.recv[p.rank],
-                        own ? i : static_cast<uint64_t>(r) * p.slot_groups * kVec + j, x[r]);
-      }
-#pragma unroll
-      for (int v = 0; v < kVec; ++v) acc[v] = x[0][v];
-#pragma unroll
-      for (int r = 1; r < M; ++r)
-#pragma unroll
-        for (int v = 0; v < kVec; ++v) acc[v] = add_rn(acc[v], x[r][v]);
-      if (p.shard_only) {
-        store8<CDT, Acc>(p.bufs[p.rank], i, acc);
-      } else {
-#pragma unroll
-        for (int r = 0; r < M; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
-      }
-    } else {
-      for (int r = 0; r < m; ++r) {
-        Acc x[kVec];
-        const bool own = (r == p.rank);
-        load8<CDT, Acc>(own ? p.bufs[r] : p.recv[p.rank],
-                        own ? i : static_cast<uint64_t>(r) * p.slot_groups * kVec + j, x);
-#pragma unroll
-        for (int v = 0; v < kVec; ++v) acc[v] = (r == 0) ? x[v] : add_rn(acc[v], x[v]);
-      }
-      if (p.shard_only) store8<CDT, Acc>(p.bufs[p.rank], i, acc);
-      else
-        for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], i, acc);
-    }
-  }
-}
-
 // SGD over bucket groups [a, b) of shard `owner` through the entries
 // (bucket-group coordinates).  shard_only: the reduced gradient of another
 // owner's shard is read from that owner's bucket over NVLink.
@@ -798,16 +720,14 @@ __device__ __forceinline__ void p2p_update_range(const P2PParams& p, int owner, 
   }
 }
 
-template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false, bool PUSH = false>
+template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
   const uint64_t T = p.groups;
   const uint64_t G = gridDim.x, c = blockIdx.x;
-  if constexpr (PUSH) p2p_push_chunks<CDT>(p);
   pair_barrier(p, 0);
   {
     const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
     if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
-    else if constexpr (PUSH) p2p_push_reduce_chunk<CDT, M>(p, s0, s0 + L * c / G, s0 + L * (c + 1) / G);
     else p2p_reduce_chunk<CDT, M>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
   }
   auto update_shard = [&](int s) {
@@ -1489,11 +1409,6 @@ uint64_t p2p_shard_elems(uint64_t count, int nranks) {
   return (count / kVec + nranks - 1) / nranks * kVec;
 }
 
-size_t p2p_recv_bytes(uint64_t count, int cdt, int nranks) {
-  const uint64_t slot_groups = (count / kVec + nranks - 1) / nranks;
-  return static_cast<size_t>(nranks) * slot_groups * kVec * dtype_size(cdt);
-}
-
 // The grid is a pure function of (groups, nranks): identical on every rank,
 // as the per-CTA pairing requires; <= 2 CTAs per SM so the cooperative launch
 // fits beside the other lanes' kernels.
@@ -1517,12 +1432,6 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     if (!a.mc && !aligned16(a.bufs[r])) throw UsageError("p2p_allreduce: bucket not 16-byte aligned");
   }
   p.mc = a.mc;
-  const bool push = !a.mc && a.recv[0];
-  for (int r = 0; push && r < a.nranks; ++r) {
-    p.recv[r] = a.recv[r];
-    if (!aligned16(a.recv[r])) throw UsageError("p2p_allreduce: receive area not 16-byte aligned");
-  }
-  p.slot_groups = (a.count / kVec + a.nranks - 1) / a.nranks;
   if (a.mc && !aligned16(a.mc)) throw UsageError("p2p_allreduce: multicast bucket not 16-byte aligned");
   p.tab = a.tab;
   p.n_entries = a.n_entries;
@@ -1568,28 +1477,6 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   CSB_P2P_PICK(CS_F64, CS_F64, true, false)
   CSB_P2P_PICK(CS_F64, CS_F64, true, true)
 #undef CSB_P2P_PICK
-  if (push) {  // writes-only NVLink traffic through the receive areas
-    fn = nullptr;
-#define CSB_PUSH_PICK(C, W, U, MO)                                                                  \
-  if (a.cdt == C && (!U || a.wdt == W) && upd == U && (!U || mom == MO)) {                          \
-    switch (a.nranks) {                                                                             \
-      case 2: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 2, false, true>); break;  \
-      case 4: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 4, false, true>); break;  \
-      case 8: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 8, false, true>); break;  \
-      default: fn = reinterpret_cast<const void*>(p2p_allreduce_kernel<C, W, U, MO, 0, false, true>); break; \
-    }                                                                                               \
-  }
-    CSB_PUSH_PICK(CS_F32, CS_F32, false, false)
-    CSB_PUSH_PICK(CS_BF16, CS_F32, false, false)
-    CSB_PUSH_PICK(CS_F64, CS_F64, false, false)
-    CSB_PUSH_PICK(CS_F32, CS_F32, true, false)
-    CSB_PUSH_PICK(CS_F32, CS_F32, true, true)
-    CSB_PUSH_PICK(CS_BF16, CS_F32, true, false)
-    CSB_PUSH_PICK(CS_BF16, CS_F32, true, true)
-    CSB_PUSH_PICK(CS_F64, CS_F64, true, false)
-    CSB_PUSH_PICK(CS_F64, CS_F64, true, true)
-#undef CSB_PUSH_PICK
-  }
   if (a.mc) {  // in-switch reduction through the multicast VA
     fn = nullptr;
 #define CSB_NVLS_PICK(C, W, U, MO)                                                                       \

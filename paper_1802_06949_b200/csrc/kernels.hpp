@@ -67,8 +67,6 @@ struct P2PArgs {
   void* bufs[CS_MAX_RANKS];
   uint32_t* flags[CS_MAX_RANKS];
   void* mc = nullptr;  // NVLS multicast VA of the bucket: in-switch reduction instead of peer loads
-  // push mode (recv[0] != nullptr): every rank's receive area, >= p2p_recv_bytes(count, cdt, nranks)
-  void* recv[CS_MAX_RANKS] = {};
   int nranks = 0, rank = 0;
   uint64_t count = 0;  // bucket elements, multiple of 8
   int cdt = CS_F32, wdt = CS_F32;
@@ -85,7 +83,6 @@ struct P2PArgs {
   double lr = 0, rescale = 0, momentum = 0;
 };
 size_t p2p_flag_bytes();
-size_t p2p_recv_bytes(uint64_t count, int cdt, int nranks);
 // elements of the largest shard of a `count`-element bucket (a multiple of 8)
 uint64_t p2p_shard_elems(uint64_t count, int nranks);
 int p2p_grid(uint64_t groups, int nranks);

@@ -137,11 +137,6 @@ std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int n
       nvls = nvls && (v & 2);
     }
     t->p2p_ok_ = ok;
-    // push mode (writes-only NVLink traffic) measured slower than peer loads
-    // on B200 (tools/nvlink_probe.cu); opt in with CSB_P2P_PUSH=1,
-    // identically on every rank
-    const char* pe = std::getenv("CSB_P2P_PUSH");
-    t->push_ = pe && std::string(pe) == "1";
     t->nvls_ok_ = ok && nvls;
     t->name_ = name;
     if (ok) t->setup_flags();
@@ -212,29 +207,6 @@ void Transport::setup_flags() {
   flags_.push_back(share_buffer(f));
 }
 
-// Called at the same matched op on every rank (the ledger matched the bucket
-// signature first), so the growth and its IPC exchange are collective.  Old
-// areas stay mapped until the transport closes: a peer may still hold them.
-void Transport::ensure_recv(int comm, size_t bytes) {
-  {
-    std::lock_guard<std::mutex> lock(mu_);
-    if (recv_bytes_.size() <= static_cast<size_t>(comm)) {
-      recv_bytes_.resize(static_cast<size_t>(comm) + 1, 0);
-      recv_.resize(static_cast<size_t>(comm) + 1);
-    }
-    if (recv_bytes_[static_cast<size_t>(comm)] >= bytes) return;
-  }
-  const size_t grown = (bytes + (2u << 20) - 1) / (2u << 20) * (2u << 20);
-  CSB_CUDA(cudaSetDevice(device_));
-  void* r = nullptr;
-  CSB_CUDA(cudaMalloc(&r, grown));
-  std::vector<void*> peers = share_buffer(r);
-  std::lock_guard<std::mutex> lock(mu_);
-  own_recv_.push_back(r);
-  recv_[static_cast<size_t>(comm)] = std::move(peers);
-  recv_bytes_[static_cast<size_t>(comm)] = grown;
-}
-
 void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
                               int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
                               void* mc) {
@@ -250,8 +222,6 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     t = ledger_->arrive(comm, rank, sig, trace_key, bucket);
   }
   if (t.last) ledger_->finish(t);
-  const bool push = push_ && !mc;
-  if (push) ensure_recv(comm, p2p_recv_bytes(count, dtype, num_ranks()));
   P2PArgs a;
   {
     std::lock_guard<std::mutex> lock(mu_);
@@ -259,7 +229,6 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     for (int r = 0; r < num_ranks(); ++r) {
       a.bufs[r] = peer_bufs[r];
       a.flags[r] = static_cast<uint32_t*>(flags_[static_cast<size_t>(comm)][static_cast<size_t>(r)]);
-      if (push) a.recv[r] = recv_[static_cast<size_t>(comm)][static_cast<size_t>(r)];
     }
   }
   a.mc = mc;
@@ -294,7 +263,6 @@ Transport::~Transport() {
     cudaSetDevice(device_);
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (void* p : own_flags_) cudaFree(p);
-    for (void* p : own_recv_) cudaFree(p);
     for (ncclComm_t c : comms_) {
       if (!c) continue;
       if (aborted) ncclCommAbort(c);

@@ -122,12 +122,6 @@ class Transport {
   std::vector<void*> ipc_opened_;
   std::vector<void*> own_flags_;
   std::vector<std::vector<void*>> flags_;  // comm -> every rank's flag region
-  // push mode: comm -> every rank's receive area (grown collectively, never shrunk)
-  void ensure_recv(int comm, size_t bytes);
-  bool push_ = false;
-  std::vector<std::vector<void*>> recv_;
-  std::vector<size_t> recv_bytes_;
-  std::vector<void*> own_recv_;
 };
 
 }  // namespace csb
