@@ -225,3 +225,56 @@ def test_large_sum_linearity_and_checksum(gpu):
     idx = np.random.default_rng(1).integers(0, n, size=1000)
     hb = [b.cpu().numpy()[idx] for b in bufs]
     np.testing.assert_array_equal(out.cpu().numpy()[idx], O.rank_order_sum(hb, "f64"))
+
+
+# ------------------------------------------------------- guard regions (OOB)
+
+@pytest.mark.parametrize("dt", ["f64", "f32", "bf16"])
+def test_kernels_never_write_outside_their_keys(gpu, dt):
+    """compute-sanitizer is closed on the pool, so out-of-bounds writes are
+    checked with canaries: every destination key of kernels (a), (b), (c)
+    sits inside one buffer between guard gaps at odd element offsets (tails
+    not a multiple of 8, unaligned keys: the scalar paths), and every guard
+    element must come back bit-identical."""
+    from paper_1802_06949_b200 import api
+    code = {"f64": api.F64, "f32": api.F32, "bf16": api.BF16}[dt]
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    sizes, gap = [1, 7, 9, 63, 1000, 4097, 70001], 37
+    offs, o = [], 5
+    for n in sizes:
+        offs.append(o)
+        o += n + gap
+    total = o
+    guard = torch.full((total,), -1234.5, device="cuda", dtype=tdt)
+    mask = torch.ones(total, dtype=torch.bool, device="cuda")
+    for off, n in zip(offs, sizes):
+        mask[off:off + n] = False
+
+    def check(buf):
+        torch.cuda.synchronize()
+        assert torch.equal(buf[mask], guard[mask]), "a kernel wrote into a guard gap"
+
+    s = stream()
+    # (a) pack into the guarded buffer
+    dst = guard.clone()
+    src = [torch.randn(n, device="cuda").to(tdt) for n in sizes]
+    api.pack([(x.data_ptr(), dst[off:].data_ptr(), n) for x, off, n in zip(src, offs, sizes)], code, code, s)
+    check(dst)
+    for x, off, n in zip(src, offs, sizes):
+        assert torch.equal(dst[off:off + n], x)
+    # (c) SGD (+ momentum) on guarded weights and momentum
+    wdt, mdt = (api.F64, torch.float64) if dt == "f64" else (api.F32, torch.float32)
+    w = torch.full((total,), -1234.5, device="cuda", dtype=torch.float64 if dt == "f64" else torch.float32)
+    v = torch.full((total,), -1234.5, device="cuda", dtype=mdt)
+    wguard = w.clone()
+    g = [torch.randn(n, device="cuda").to(tdt) for n in sizes]
+    api.sgd_update([(w[off:].data_ptr(), x.data_ptr(), v[off:].data_ptr(), n) for x, off, n in zip(g, offs, sizes)],
+                   wdt, code, 0.1, 0.01, 0.9, s)
+    torch.cuda.synchronize()
+    assert torch.equal(w[mask], wguard[mask]) and torch.equal(v[mask], wguard.to(mdt)[mask])
+    # (b) rank-order sum into a guarded output slice (one key at a time)
+    out = guard.clone()
+    for off, n in zip(offs, sizes):
+        ins = [torch.randn(n, device="cuda").to(tdt) for _ in range(3)]
+        api.sum_buffers([x.data_ptr() for x in ins], [out[off:].data_ptr()], n, code, s)
+    check(out)
