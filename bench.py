@@ -169,6 +169,25 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture of this exact workload
+    (profiles/r1b_<kernel>_raw.csv, ResNet-50 DepCha 100 MiB, N=1), or None."""
+    import csv
+    path = ROOT / "profiles" / f"r1b_{kernel}_raw.csv"
+    try:
+        rows = list(csv.reader(path.open()))
+        head, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        total = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = head.index(k)
+            total += float(vals[i].replace(",", "")) * scale[units[i]]
+        return {"bytes": int(total), "source": f"profiles/{path.name} (ncu --set full, one launch)"}
+    except Exception:
+        return None
+
+
 def peaks() -> dict:
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -399,8 +418,12 @@ def main():
             peak_source = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"
         avg_s = ks["total_ms"] / max(1, ks["launches"]) / 1e3
         achieved = bytes_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+        traffic = (ncu_traffic(f"{dom}_tab_kernel") if (bound == "hbm" and args.config == "resnet50"
+                                                       and bucket_mb == 100 and world == 1) else None)
         line["roofline"] = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                            "unit": "GB/s", "frac": round(achieved / peak, 4),
+                            "traffic": traffic["bytes"] if traffic else None,
+                            "traffic_source": traffic["source"] if traffic else None,
                             "launches": ks["launches"],
                             "avg_launch_us": round(1000 * ks["total_ms"] / max(1, ks["launches"]), 2),
                             "bytes_per_launch": round(bytes_launch),
