@@ -14,6 +14,12 @@ read like the reference's own tests:
         .init(key, slot) / .push(keys, slots) / .pull(keys, slots)
         .pull_update(keys, slots, lr, rescale, momentum) / .barrier() / .comm_buf(key)
 
+B200 extensions: KvConfig(bucket_bytes, issue_order, comm_dtype, p2p=1 (fused
+NVLink allreduce+update kernel) / 2 (NVLS), zero=1 (ZeRO-1)),
+KvStore.bucket_view[_tensor] (gradient-as-bucket-view), Engine.import_event /
+stream_wait (a framework's own CUDA stream as producer / consumer),
+Transport.allreduce_p2p / allreduce_nvls, SynthModel (the bench's trainer).
+
 Device buffers are torch tensors (plumbing only); everything they are handed
 to runs in libcollsim_b200.so.
 """
