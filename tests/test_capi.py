@@ -104,3 +104,25 @@ def test_kvstore_config_validation_before_any_device_work():
         KvStore(eng, tr, 0, KvConfig("depcha", 1, 4))
     eng.close()
     tr.close()
+
+
+def test_interop_and_peer_memory_entry_points_reject_misuse_without_a_gpu():
+    """The B200 entry points fail with status codes, never crash: a null
+    framework event, stream ops on a host-only engine, peer-memory / NVLS
+    collectives on a transport that has no peer path."""
+    from paper_1802_06949_b200 import Engine, Transport, UsageError, api
+    e = Engine(1)  # host-only
+    t = e.new_variable()
+    with pytest.raises(UsageError, match="null event"):
+        e.import_event(0, [t])
+    e.stream_wait([t], 0)  # nothing pushed on the tag: nothing to wait for
+    tr = Transport.ledger_only(2)
+    assert not tr.p2p_capable() and not tr.nvls_capable()
+    with pytest.raises(UsageError, match="peer-memory"):
+        tr.share_buffer(0x1000)
+    with pytest.raises(UsageError):
+        tr.allreduce_p2p(0, 0, [0x1000, 0x2000], 64, api.F32)
+    with pytest.raises(UsageError):
+        tr.alloc_nvls(1 << 20)
+    tr.close()
+    e.close()
