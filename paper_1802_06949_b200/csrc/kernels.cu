@@ -7,10 +7,20 @@
 //                        (collective.cpp:228-236: acc = b0; acc += b1 ...; copy to all)
 //   (c) cs_sgd_update  : fused unpack + rescale + SGD / momentum update
 //                        (model.cpp:17-27, trainer.cpp:74-80)
+//   p2p_allreduce_kernel / p2p_zero_kernel
+//                      : (b)+(c) fused over CUDA-IPC peer memory or an NVSwitch
+//                        multicast VA, one cooperative launch per bucket,
+//                        rank-order sums, pair barriers per CTA; the ZeRO-1
+//                        form updates a sharded master and all-gathers weights
 //   cs_synth_backward  : synthetic per-key backward producer (bench only)
 //   cs_checksum        : deterministic fp64 checksum (e2e result read-back)
 //
-// Design (B200, HBM-bound, no tensor cores):
+// Sections: vector IO | table lookup | (a) pack | (b) sum | (c) update |
+// device-resident tables | fused NVLink allreduce | ZeRO-1 | synthetic
+// backward | checksum | host side (launch accounting, launchers) | API |
+// DeviceTable.
+//
+// Design of the streaming kernels (B200, HBM-bound, no tensor cores):
 //   * 256-thread CTAs; a thread moves groups of 8 elements as 16-byte
 //     vectors (ld/st .v4 / .v2.f64), 2-4 groups unrolled with every load
 //     issued before the first store (>= 64 B in flight per thread).
