@@ -76,13 +76,20 @@ class KvStore {
   KvStore(const KvStore&) = delete;
   KvStore& operator=(const KvStore&) = delete;
 
+  // kvstore.cpp:76-97: keys densely in order; rank 0's weights broadcast.
   void init(int key, TensorSlot weights);
+  // kvstore.cpp:99-143 / 145-183, one key (the reference calls) or a list
+  // (one pack / one collective per fusion bucket).
   void push(int key, TensorSlot grad) { push(std::vector<int>{key}, std::vector<TensorSlot>{grad}); }
   void pull(int key, TensorSlot out) { pull(std::vector<int>{key}, std::vector<TensorSlot>{out}); }
   void push(const std::vector<int>& keys, const std::vector<TensorSlot>& grads);
   void pull(const std::vector<int>& keys, const std::vector<TensorSlot>& outs);
+  // pull fused with sgd_update (model.cpp:17-27; + momentum): the update reads
+  // the reduced bucket directly; with p2p, DepCha does the allreduce and the
+  // update in ONE kernel (ZeRO-1 with cfg.zero).
   void pull_update(const std::vector<int>& keys, const std::vector<TensorSlot>& weights,
                    const SgdConfig& sgd);
+  // kvstore.cpp:185-193 (ConCom: drain the window, then a world barrier).
   void barrier();
 
   int rank() const { return rank_; }
