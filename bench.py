@@ -486,7 +486,10 @@ def main():
         e2e_step = wall / args.steps
         line["e2e"] = {"value": round(world * gbytes / (e2e_step * 1e6), 3), "unit": "GB/s",
                        "h2d_bytes_per_step": model_e2e.info()["h2d_bytes_per_step"], "d2h_bytes_per_step": 8,
-                       "ms_per_step": round(e2e_step, 4)}
+                       "ms_per_step": round(e2e_step, 4),
+                       "note": "wall clock through the C ABI: per step one pinned-host H2D of the gradients, "
+                               "the step, a weight checksum read back D2H; the host reads step i's result "
+                               "after queueing step i+1"}
         model_e2e.close()
 
         # ---- CPU baseline: the reference on this host, bounded sample

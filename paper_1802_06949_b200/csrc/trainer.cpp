@@ -139,8 +139,8 @@ void SynthModel::init() {
     CSB_CUDA(cudaMalloc(&src_arena_, gtot));
     CSB_CUDA(cudaMemcpy(src_arena_, gh.data(), gtot, cudaMemcpyHostToDevice));
   }
-  CSB_CUDA(cudaMalloc(&sum_dev_, 8));
-  CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sum_host_), 8, cudaHostAllocDefault));
+  CSB_CUDA(cudaMalloc(&sum_dev_, 2 * sizeof(double)));
+  CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sum_host_), 2 * sizeof(double), cudaHostAllocDefault));
   w_arena_elems_ = wtot / ws;
   g_arena_bytes_ = gtot;
 
@@ -179,7 +179,8 @@ void SynthModel::init() {
     wt_.push_back(engine_.new_variable());
     gt_.push_back(engine_.new_variable());
   }
-  sum_tag_ = engine_.new_variable();
+  sum_tag_[0] = engine_.new_variable();
+  sum_tag_[1] = engine_.new_variable();
   for (int k = 0; k < K; ++k)
     kv_.init(k, TensorSlot{w_[k], cfg_.wdt, cfg_.sizes[k], wt_[k]});
   engine_.wait_all();
@@ -320,14 +321,17 @@ void SynthModel::enqueue_step(int flags) {
     void* w = w_arena_;
     const uint64_t n = w_arena_elems_;
     const int wdt = cfg_.wdt;
-    double* d = sum_dev_;
-    double* h = sum_host_;
+    const int slot = sum_next_;
+    double* d = sum_dev_ + slot;
+    double* h = sum_host_ + slot;
     engine_.push_stream(
         [w, n, wdt, d, h](cudaStream_t s) {
           ::csb::checksum(w, n, wdt, d, s);
           CSB_CUDA(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, s));
         },
-        wt_, {sum_tag_}, OpKind::Copy, -1, 0, Dispatch::Inline);
+        wt_, {sum_tag_[slot]}, OpKind::Copy, -1, 0, Dispatch::Inline);
+    sum_last_ = slot;
+    sum_next_ = slot ^ 1;
   }
 }
 
@@ -366,10 +370,22 @@ double SynthModel::run(int steps, int flags) {
 double SynthModel::run_e2e(int steps, int flags) {
   engine_.wait_all();
   const auto t0 = std::chrono::steady_clock::now();
+  // every step uploads its inputs and reads its result back; the host reads
+  // step i's result after queueing step i+1 (one step of lag, as a training
+  // loop that logs the previous loss), so the next upload is not held back
+  int prev = -1;
   for (int i = 0; i < steps; ++i) {
     enqueue_step(flags | kStepChecksum);
-    engine_.wait_for(sum_tag_);  // the step's result is on the host
-    volatile double v = *sum_host_;
+    if (prev >= 0) {
+      engine_.wait_for(sum_tag_[prev]);
+      volatile double v = sum_host_[prev];
+      (void)v;
+    }
+    prev = sum_last_;
+  }
+  if (prev >= 0) {
+    engine_.wait_for(sum_tag_[prev]);  // the last step's result is on the host
+    volatile double v = sum_host_[prev];
     (void)v;
   }
   const auto t1 = std::chrono::steady_clock::now();
@@ -379,8 +395,8 @@ double SynthModel::run_e2e(int steps, int flags) {
 
 double SynthModel::checksum() {
   enqueue_step(kStepChecksum);
-  engine_.wait_for(sum_tag_);
-  return *sum_host_;
+  engine_.wait_for(sum_tag_[sum_last_]);
+  return sum_host_[sum_last_];
 }
 
 }  // namespace csb

@@ -89,9 +89,13 @@ class SynthModel {
   uint64_t g_arena_bytes_ = 0;
   char* src_arena_ = nullptr;  // device (synthetic) or pinned host (e2e)
   void* h2d_dst_ = nullptr;    // e2e upload target: the gradient arena, or the bucket arena (views)
+  // two checksum slots, so the host can read step t's result while step t+1
+  // is already queued (run_e2e)
   double* sum_dev_ = nullptr;
   double* sum_host_ = nullptr;
-  Tag sum_tag_;
+  Tag sum_tag_[2];
+  int sum_next_ = 0;  // slot of the next checksum
+  int sum_last_ = 0;  // slot of the last enqueued checksum
   std::vector<std::vector<int>> groups_;
   std::vector<void*> mom_local_;  // momentum of the no-kvstore update path
   double last_host_ms_ = 0.0;
