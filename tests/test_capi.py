@@ -1,7 +1,6 @@
 """The drop-in boundary: libcollsim_b200.so loads (no GPU needed) and exports
 every entry point include/collsim_b200.h declares; status codes map to the
 reference error kinds (R/core/include/collsim/error.hpp:10-31).  CPU only."""
-import ctypes as C
 import re
 import subprocess
 from pathlib import Path

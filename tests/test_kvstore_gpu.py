@@ -3,7 +3,6 @@ transport: kernel (b) reduces in rank order on HBM).  Ports of the reference's
 test_kvstore.cpp / acceptance.cpp cases plus parity against golden fixtures
 frozen from the reference itself (tests/golden/make_golden.py)."""
 import json
-import threading
 from pathlib import Path
 
 import numpy as np
