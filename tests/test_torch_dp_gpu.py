@@ -102,7 +102,6 @@ def test_torch_producer_bucket_views(gpu, momentum):
         y = torch.randint(0, 10, (32,), device="cuda", generator=gen)
         dp.zero_grad()
         torch.nn.functional.cross_entropy(model(x), y).backward()
-        g = None
         dp.step()
         torch.cuda.synchronize()
         g = _flat([p.grad for p in dp.params])  # 1 rank: the in-place "sum" is the gradient itself
