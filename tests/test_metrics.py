@@ -55,3 +55,15 @@ def test_primary_error_priority():
     assert primary_error(["EngineError", "UsageError"]) == "UsageError"
     assert primary_error(["DeadlockTimeout", "MismatchError", "UsageError"]) == "MismatchError"
     assert primary_error(["CudaError", "EngineError"]) == "EngineError"
+
+
+def test_run_config_validation_before_any_work():
+    """runner.cpp:16-34 `validate`: every bad run configuration is a
+    ConfigError raised before a transport or a GPU is touched."""
+    from paper_1802_06949_b200.metrics import run_synthetic
+    bad = [dict(workers=0), dict(engine_threads=0), dict(epochs=0), dict(global_batch=0),
+           dict(workers=3, global_batch=64), dict(mode="concom", outstanding=0), dict(inject_latency_us=-1)]
+    msgs = ["workers", "engine-threads", "epochs", "divide evenly", "divide evenly", "outstanding", "latency"]
+    for kw, msg in zip(bad, msgs):
+        with pytest.raises(ConfigError, match=msg):
+            run_synthetic(**kw)
