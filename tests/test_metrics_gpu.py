@@ -132,3 +132,13 @@ def test_cli_run_emits_reference_metrics(gpu, tmp_path, mode):
     assert m.ok() and m.mode == mode and m.model == "diamond" and len(m.epoch_times_s) == 2
     assert metrics_from_json(mpath.read_text()) == m
     assert tpath.stat().st_size > 0
+
+
+def test_runs_are_deterministic(gpu):
+    """test_harness.cpp 'loss and accuracy are deterministic across repeated
+    runs': two identical GPU runs end with bit-identical weights on every rank."""
+    kw = dict(mode="depcha", workers=2, epochs=1, steps_per_epoch=3, sizes=[64, 1000, 4096, 7, 300],
+              backward_ms=0.1, momentum=0.9)
+    a, b = run_synthetic(**kw), run_synthetic(**kw)
+    assert a.ok() and b.ok()
+    assert a.b200["weight_checksums"] == b.b200["weight_checksums"]
