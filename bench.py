@@ -1,45 +1,56 @@
 #!/usr/bin/env python
-"""bench.py -- aggregated gradient GB/s and exposed comm ms/iter (BASELINE.json).
+"""bench.py -- aggregated gradient GB/s/GPU & exposed comm ms/iter (BASELINE.json).
 
 Workload (N=1 default, BASELINE.json configs[1]): the ResNet-50 gradient set
 (161 keys, 25,557,032 fp32 params, torchvision parameter order) under DepCha,
-fusion buckets of 25 MiB grouped in gradient-ready (descending) order, SGD
-with momentum 0.9.  One "step" = one pass of the hot path over every key:
-push (kernel (a) packs each bucket) -> allreduce (NCCL, one ordered stream,
-chained by the DepCha dummy tag) -> fused pull+update (kernel (c) reads the
-reduced bucket and updates weights + momentum in place).
+one 100 MiB fusion bucket in gradient-ready (descending) order, SGD with
+momentum 0.9.  One "step" = one pass of the hot path over every key: push
+(kernel (a) packs the gradients into the bucket) -> allreduce (the identity
+at N=1; at N>1 the fused peer-memory kernel: rank-order reduce-scatter over
+NVLink + SGD/momentum update + all-gather, ZeRO-1 for fp32 sets) -> fused
+pull+update (kernel (c)).
 
-  value          whole-job aggregated gradient GB/s = N x gradient bytes per
-                 rank / device step time (max over ranks), gradients resident
-                 in HBM; inputs (gradients + weights + momentum + buckets,
-                 ~409 MB/rank) exceed the 126 MB L2, so no flush is needed.
-  e2e            same metric through the C-ABI with HOST buffers: every step
-                 copies the gradients H2D from pinned memory, runs the path,
-                 and reads the weight checksum back D2H (wall clock).
+  value          aggregated gradient GB/s PER GPU (the metric's unit) =
+                 gradient bytes per rank / device step time (max over ranks);
+                 gradients resident in HBM, working set (~409 MB/rank) > the
+                 126 MB L2, so no flush is needed.  `whole_job_gbs` = N x value.
+  e2e            the same metric through the C ABI with HOST buffers: every
+                 step copies the gradients H2D from pinned memory, runs the
+                 path and reads the weight checksum back D2H (wall clock).
   exposed_comm   T(synthetic backward + aggregation) - T(synthetic backward +
                  local update), per iteration, CUDA events, max over ranks.
-  roofline       dominant kernel of the step, CUDA-event timed per launch on
-                 its own stream, algorithmic bytes / duration vs measured HBM.
+  roofline       dominant kernel, CUDA-event timed per launch on its stream,
+                 algorithmic bytes / duration vs measured HBM (N=1) or NVLink.
+  parity         a fresh model of the same config, 3 steps, weights read back
+                 and checked against the CPU oracle (the checker, oracle.c
+                 or_synth_expect, pinned to the reference's golden weights):
+                 bit-exact vs the fp32 restatement, max relative error vs fp64.
+  f64            the same step in the reference's own arithmetic (fp64
+                 weights and gradients, plain SGD), bit-exact vs the reference.
   cpu_baseline   the reference (oracle/_ref, compiled from /root/reference)
                  timed on this host's cores on a bounded sample (rank 0, N=1).
 
-`--impl reference` times the reference's own CPU path (oracle/_ref) instead.
-For N > 1 launch with torchrun; one process per GPU, NCCL between them.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, NCCL between them) and fails if fewer than N GPUs are
+visible.  `--impl reference` times the reference's own CPU path instead
+(rank 0 only; R = N rank threads), with the identical `config`.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
+import zlib
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
-sys.path.insert(0, str(ROOT))
 
 METRIC = "aggregated gradient GB/s/GPU & exposed comm ms/iter at 1/2/4/8 B200"
 CONFIGS = {
@@ -52,6 +63,17 @@ CONFIGS = {
     "uniform16": ("uniform16x1048576", "funnel", 1, "fp32", 0, 0.0),
 }
 CALIB = ROOT / "paper_1802_06949_b200" / "calibration"
+ELEM = {"fp32": 4, "bf16": 2, "fp64": 8}
+
+
+def load_keys(keyset: str) -> list[int]:
+    """Key sizes from paper_1802_06949_b200/keysets.py, loaded as a plain
+    module file: the reference arm must not import the package (which maps
+    libcollsim_b200.so)."""
+    spec = importlib.util.spec_from_file_location("_csb_keysets", ROOT / "paper_1802_06949_b200" / "keysets.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.load(keyset)
 
 
 def backward_profile(spec, keys):
@@ -82,6 +104,8 @@ def parse():
     p.add_argument("--backward-ms", type=float, default=None)
     p.add_argument("--engine-threads", type=int, default=4)
     p.add_argument("--no-extras", action="store_true", help="headline only (no e2e/exposed/roofline/cpu)")
+    p.add_argument("--no-parity", dest="parity", action="store_false")
+    p.add_argument("--parity-steps", type=int, default=3)
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-zero", dest="zero", action="store_false",
                    help="replicated optimizer state instead of ZeRO-1 (the fused kernel's default at N>1 for "
@@ -100,6 +124,31 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: one process per GPU through
+    torch.distributed.run (rendezvous on 127.0.0.1).  Returns the child's exit
+    code, or None when this process is already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {n} CUDA device(s) visible"}),
+              flush=True)
+        return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 class Clocks:
@@ -169,23 +218,31 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+# committed `ncu --set full` captures of the N=1 headline workload, newest first
+NCU_CAPTURES = ["r2", "r1b"]
+
+
 def ncu_traffic(kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed `ncu --set full` capture of this exact workload
-    (profiles/r1b_<kernel>_raw.csv, ResNet-50 DepCha 100 MiB, N=1), or None."""
+    (profiles/<round>_<kernel>_raw.csv, ResNet-50 DepCha 100 MiB, N=1), or None."""
     import csv
-    path = ROOT / "profiles" / f"r1b_{kernel}_raw.csv"
-    try:
-        rows = list(csv.reader(path.open()))
-        head, units, vals = rows[0], rows[1], rows[2]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        total = 0.0
-        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            i = head.index(k)
-            total += float(vals[i].replace(",", "")) * scale[units[i]]
-        return {"bytes": int(total), "source": f"profiles/{path.name} (ncu --set full, one launch)"}
-    except Exception:
-        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for tag in NCU_CAPTURES:
+        path = ROOT / "profiles" / f"{tag}_{kernel}_raw.csv"
+        if not path.exists():
+            continue
+        try:
+            rows = list(csv.reader(path.open()))
+            head, units, vals = rows[0], rows[1], rows[2]
+            total = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = head.index(k)
+                total += float(vals[i].replace(",", "")) * scale[units[i]]
+            return {"bytes": int(total), "source": f"profiles/{path.name} (ncu --set full, one launch)"}
+        except Exception:
+            continue
+    return None
 
 
 def peaks() -> dict:
@@ -195,88 +252,167 @@ def peaks() -> dict:
         return {}
 
 
+def workload(args):
+    keyset, mode, outstanding, dtype, bucket_mb, bwd_spec = CONFIGS[args.config]
+    mode = args.mode or mode
+    outstanding = args.outstanding or outstanding
+    bucket_mb = args.bucket_mb if args.bucket_mb is not None else bucket_mb
+    return keyset, mode, outstanding, dtype, bucket_mb, bwd_spec
+
+
+def config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world) -> dict:
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
+            "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
+            "issue_order": args.issue_order, "momentum": args.momentum, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (no flush)",
+            "producer_order": "per-rank random (seeded)" if args.config == "stress" else "reverse key order",
+            "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
+            else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)",
+            "step": "push + allreduce + pull/SGD update over every key (trainer.cpp:112-141), no backward",
+            "value_basis": f"gradient bytes per rank = params x {ELEM[dtype]} B ({dtype}) per step time, per GPU"}
+
+
 # ------------------------------------------------------------- reference
 
-def run_reference(args, keys, mode, outstanding, world, warmup=1, iters=None):
-    """The reference's own CPU path (Engine + KvStore + Transport, compiled
-    from /root/reference into oracle/_ref) on the host cores."""
-    sys.path.insert(0, str(ROOT / "tests"))
+def ref_lib():
+    """The unmodified reference (oracle/_ref/libcollsim_ref.so, compiled from
+    /root/reference by oracle/Makefile), loaded on its own: nothing of this
+    package and not the oracle restatement."""
     import ctypes as C
-    import _oracle as O  # checker / reference loader (test infrastructure)
+    so = ROOT / "oracle" / "_ref" / "libcollsim_ref.so"
+    if not so.exists():
+        return None
+    lib = C.CDLL(str(so))
+    lib.ref_last_error.restype = C.c_char_p
+    lib.ref_bench.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                              C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p]
+    return lib
 
-    R = O.ref_lib()
+
+def run_reference(keys, mode, outstanding, ranks, warmup, iters, elem_bytes):
+    """The reference's own CPU path (Engine + KvStore + Transport) on the host
+    cores: R rank threads x T engine threads, fp64 (its only dtype), the same
+    push / pull / sgd loop as the GPU step (ref_driver.cpp ref_bench)."""
+    import ctypes as C
+    R = ref_lib()
     if R is None:
         return None
     ncores = os.cpu_count() or 1
-    ranks = max(1, world)
     threads = max(2, ncores // ranks)
     sizes = (C.c_int64 * len(keys))(*keys)
     stats = (C.c_double * 2)()
-    iters = args.cpu_steps if iters is None else iters
+    rescale = 1.0 / (64 * ranks)
     rc = R.ref_bench(mode.encode(), ranks, threads, outstanding, len(keys), sizes, warmup, iters, 0,
-                     0.1, 1.0 / (64 * ranks), stats)
+                     0.1, rescale, stats)
     if rc != 0:
         raise RuntimeError(R.ref_last_error().decode())
     ms = stats[0]
-    bytes_rank = stats[1]
-    return {"ms_per_step": ms, "value": ranks * bytes_rank / (ms * 1e6), "per_rank": bytes_rank / (ms * 1e6),
-            "cores": min(ncores, ranks * (threads + 1)), "ranks": ranks, "threads": threads,
-            "bytes_per_rank": bytes_rank}
+    gbytes = sum(keys) * elem_bytes
+    return {"ms_per_step": ms, "per_gpu": gbytes / (ms * 1e6), "cores": min(ncores, ranks * (threads + 1)),
+            "ranks": ranks, "threads": threads, "fp64_bytes_per_rank": stats[1]}
 
 
-def reference_main(args, cfg_name, keys, mode, outstanding, config):
+def reference_main(args, keys, mode, outstanding, dtype, bucket_mb):
     rank, _, world = dist_env()
+    ranks = world if "WORLD_SIZE" in os.environ else args.gpus
     if rank != 0:
-        return
-    # the driver's --steps / --warmup, bounded so the arm stays within a few
-    # minutes on the host cores (one fp64 ResNet-50 step is ~0.1-2 s)
-    warmup, steps = max(1, min(args.warmup, 3)), max(1, min(args.steps, 10))
-    ref = run_reference(args, keys, mode, outstanding, world, warmup, steps)
+        return 0  # rank 0 runs all R rank threads of the reference on the host
+    config = config_dict(args, keys, mode, outstanding, dtype, bucket_mb, ranks)
+    ref = run_reference(keys, mode, outstanding, ranks, args.warmup, args.steps, ELEM[dtype])
     if ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcollsim_ref.so not built"}))
-        return
+        return 0
+    v = round(ref["per_gpu"], 4)
+    sample = (f"{len(keys)} keys, {ranks} rank thread(s) x {ref['threads']} engine threads, fp64 arithmetic, "
+              f"{args.steps} steps after {args.warmup} warm-up (the driver's --steps/--warmup)")
     line = {
-        "metric": METRIC, "impl": "reference", "value": round(ref["value"], 4), "unit": "GB/s",
-        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": round(ref["ms_per_step"], 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": METRIC, "impl": "reference", "value": v, "unit": "GB/s", "n_gpus": ranks, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ref["ms_per_step"], 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (random_uniform seeds 1000+r*K+k)", "config": config,
-        "cpu_baseline": {"value": round(ref["value"], 4), "unit": "GB/s", "cores": ref["cores"],
-                         "kind": "reference",
-                         "sample": f"{len(keys)} keys, {ref['ranks']} rank threads x {ref['threads']} engine "
-                                   f"threads, fp64, {steps} iterations after {warmup} warm-up "
-                                   f"(--steps/--warmup capped at 10/3 for the CPU arm)"},
-        "e2e": {"value": round(ref["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "whole_job_gbs": round(v * ranks, 4),
+        "reference_arithmetic": "fp64 plain SGD (model.cpp:17-27 has no momentum); value counts the config's "
+                                f"gradient bytes ({ELEM[dtype]} B/param) so both arms' GB/s measure the same "
+                                "work -- the reference moves fp64 (8 B/param)",
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": ref["cores"], "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- parity
+
+def parity_check(api, engine, transport, rank, world, keys, kw, comms, gdt, steps, barrier, dist):
+    """A fresh model of the benchmarked config runs `steps` steps (synthetic
+    backward + aggregation), its weights are read back and compared with the
+    CPU oracle -- the checker, oracle.c or_synth_expect, itself pinned to the
+    reference's golden weights (tests/test_oracle.py).  Rank 0 compares; every
+    rank's weight CRC must equal rank 0's.  Outside every timed region."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, str(ROOT / "tests"))
+    m = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms,
+                       **{**kw, "backward_ns": 0, "grad_views": False})
+    m.init()
+    m.run(steps, api.SynthModel.BACKWARD | api.SynthModel.COMM)
+    barrier()
+    K = len(keys)
+    # bounded check for huge key sets (C5): every 16th key
+    sel = list(range(K)) if sum(keys) <= 2**28 else list(range(0, K, 16))
+    w_all = m.read_weights()
+    m.close()
+    offs = np.concatenate([[0], np.cumsum(keys)])
+    w = np.concatenate([w_all[offs[k]:offs[k + 1]] for k in sel]) if len(sel) < K else w_all
+    crc = zlib.crc32(w.tobytes())
+    agree = True
+    if world > 1:
+        t = torch.tensor([crc, -crc], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        agree = int(t[0]) == crc and int(t[1]) == -crc
+    out = None
+    if rank == 0:
+        import _oracle as O  # the checker (test infrastructure), never on the measured path
+        wname = {api.F64: "f64", api.F32: "f32"}[kw["w_dtype"]]
+        gname = {api.F64: "f64", api.F32: "f32", api.BF16: "bf16"}[kw["g_dtype"]]
+        cname = {api.F64: "f64", api.F32: "f32", api.BF16: "bf16"}[kw["comm_dtype"]]
+        t0 = time.time()
+        exp, r64, scale = O.synth_expect(keys, world, steps, wdt=wname, gdt=gname, cdt=cname, lr=kw["lr"],
+                                         rescale=kw["rescale"], momentum=kw["momentum"],
+                                         keys=None if len(sel) == K else sel)
+        err = float(np.max(np.abs(w.astype(np.float64) - r64) / np.maximum(scale, 1e-30)))
+        tol = 1e-2 if gname == "bf16" else 1e-6
+        out = {"steps": steps, "ranks": world, "keys_checked": len(sel), "elems_checked": int(w.size),
+               "bit_exact_vs_restatement": bool(np.array_equal(w, exp)),
+               "max_rel_err_vs_f64": err, "tolerance": tol, "within_tolerance": err <= tol,
+               "ranks_agree": agree,
+               "oracle": f"oracle/oracle.c or_synth_expect ({wname} weights, {cname} sums in rank order; "
+                         f"pinned to the reference's golden weights), {time.time() - t0:.1f} s on the host"}
+    barrier()
+    return out
 
 
 # ------------------------------------------------------------------ ours
 
 def main():
     args = parse()
-    keyset, mode, outstanding, dtype, bucket_mb, bwd_spec = CONFIGS[args.config]
-    mode = args.mode or mode
-    outstanding = args.outstanding or outstanding
-    bucket_mb = args.bucket_mb if args.bucket_mb is not None else bucket_mb
-    from paper_1802_06949_b200 import keysets
-    keys = keysets.load(keyset)
+    keyset, mode, outstanding, dtype, bucket_mb, bwd_spec = workload(args)
+    keys = load_keys(keyset)
+    if args.impl == "reference":
+        return reference_main(args, keys, mode, outstanding, dtype, bucket_mb)
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    rank, local_rank, world = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     ready_ms, bwd_ms, bwd_desc = backward_profile(
         args.backward_ms if args.backward_ms is not None else bwd_spec, keys)
-    rank, local_rank, world = dist_env()
-    config = {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
-              "outstanding": outstanding, "grad_dtype": dtype, "bucket_mb": bucket_mb,
-              "issue_order": args.issue_order, "momentum": args.momentum, "parallelism": f"dp{world}",
-              "l2": "inputs larger than L2 (no flush)",
-              "producer_order": "per-rank random (seeded)" if args.config == "stress" else "reverse key order",
-              "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
-              else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"}
-    if args.impl == "reference":
-        return reference_main(args, args.config, keys, mode, outstanding, config)
+    config = config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world)
     if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
         args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
-    config["optimizer_state"] = ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
-                                 "fused kernel" if (args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32" and world > 1)
-                                 else "replicated on every rank")
+    zero_on = args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32" and world > 1
 
     import torch
     import torch.distributed as dist
@@ -303,24 +439,27 @@ def main():
 
     dt = {"fp32": api.F32, "bf16": api.BF16}[dtype]
     transport = api.Transport.nccl(name[0], world, rank, local_rank, 120000)
-    comms_main = api.create_communicators(transport, outstanding) if mode == "concom" else []
-    comms_e2e = api.create_communicators(transport, outstanding) if (mode == "concom" and not args.no_extras) else []
-    # communicators for the schedule comparison (setup-only, before any collective)
+    # every communicator is created at setup, before the first collective
+    concom = mode == "concom"
+    comms_main = api.create_communicators(transport, outstanding) if concom else []
+    comms_e2e = api.create_communicators(transport, outstanding) if (concom and not args.no_extras) else []
+    comms_par = api.create_communicators(transport, outstanding) if (concom and args.parity) else []
     sched_outstanding = 4
     comms_sched = (api.create_communicators(transport, sched_outstanding)
-                   if (world > 1 and not args.no_extras and mode != "concom") else [])
+                   if (world > 1 and not args.no_extras and not concom) else [])
     engine = api.Engine(args.engine_threads, rank, None, local_rank)
     common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
                   p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
-                  zero=args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32",
-                  order_seed=1 if args.config == "stress" else 0)
-    config["collectives"] = ("identity (1 rank)" if world == 1 else
-                             {"nccl": "NCCL",
-                              "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
-                              "nvls": "fused allreduce+update kernel, NVSwitch multicast in-switch reduction"}[args.comm])
+                  zero=zero_on, order_seed=1 if args.config == "stress" else 0)
+    path = {"collectives": ("identity (1 rank)" if world == 1 else
+                            {"nccl": "NCCL" + (f", {outstanding} concurrent communicators" if concom else ""),
+                             "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
+                             "nvls": "fused allreduce+update kernel, NVSwitch multicast in-switch reduction"}[args.comm]),
+            "optimizer_state": ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
+                                "fused kernel" if zero_on else "replicated on every rank")}
     model = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_main, ready_ms=ready_ms,
                            **common)
     model.init()
@@ -331,7 +470,8 @@ def main():
     LOCAL = api.SynthModel.LOCAL_UPDATE
 
     # ---- headline: aggregation steps, gradients resident in HBM
-    model.run(args.warmup, COMM)
+    model.run(1, BWD | COMM)  # the gradients hold this rank's values (synthetic backward once)
+    model.run(max(0, args.warmup - 1), COMM)
     barrier()
     api.host_profile(reset=True)
     l0 = api.launch_count()
@@ -356,13 +496,12 @@ def main():
     ms = max_over_ranks(ms)
     step_ms = ms / args.steps
     per_gpu = gbytes / (step_ms * 1e6)
-    value = world * per_gpu
-    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC, "value": round(per_gpu, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dtype.replace("fp", "f"),
-            "data": "synthetic (random_uniform seeds 1000+r*K+k; torchvision ResNet-50 key sizes)",
-            "config": config, "per_gpu_gbs": round(per_gpu, 3), "grad_bytes_per_rank": gbytes,
-            "buckets": info["num_buckets"], "gpu_launches": launches,
+            "data": "synthetic (random_uniform seeds 1000+r*K+k; torchvision key sizes)",
+            "config": config, "whole_job_gbs": round(world * per_gpu, 3), "grad_bytes_per_rank": gbytes,
+            "path": path, "buckets": info["num_buckets"], "gpu_launches": launches,
             "host_dispatch_ms_per_step": round(host_ms / args.steps, 4),
             "clocks": {**clk.summary(), "window": "timed region + 0.5 s of the same steps"}}
 
@@ -392,9 +531,9 @@ def main():
         # ---- roofline of the dominant kernel (CUDA events on the launch stream)
         api.profile_reset()
         api.profile_enable(True)
-        model.run(max(3, min(args.steps, 10)), COMM)
-        api.profile_enable(False)
         n_prof = max(3, min(args.steps, 10))
+        model.run(n_prof, COMM)
+        api.profile_enable(False)
         kstats = {k: api.profile_collect(k) for k in ("pack", "sum", "sgd")}
         dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
         ks = kstats[dom]
@@ -405,7 +544,6 @@ def main():
             # peer loads: (N-1)/N of the gradients in the reduce-scatter, plus
             # (N-1)/N of the reduced gradients (replicated update) or of the
             # fp32 master weights (ZeRO-1 all-gather); NVLS: 1 x bucket bytes
-            zero_on = args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32"
             second = sum(keys) * 4 if zero_on else gbytes
             link_step = ((world - 1) / world * (gbytes + second) if args.comm == "p2p" else gbytes)
             bytes_launch = link_step * n_prof / max(1, ks["launches"])
@@ -429,14 +567,14 @@ def main():
                             "bytes_per_launch": round(bytes_launch),
                             "peak_source": peak_source,
                             "kernels": {k: {"launches": v["launches"],
-                                            "ms_per_step": round(v["total_ms"] / max(3, min(args.steps, 10)), 4),
+                                            "ms_per_step": round(v["total_ms"] / n_prof, 4),
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}
                                         for k, v in kstats.items()}}
 
         # ---- the paper's three schedules on the same gradient set (N>1)
         if world > 1:
             scheds = {mode: {"value": line["value"], "ms_per_step": line["ms_per_step"],
-                             "collectives": config["collectives"]}}
+                             "collectives": path["collectives"]}}
             for sched in ("funnel", "depcha", "concom"):
                 if sched in scheds:
                     continue
@@ -449,14 +587,14 @@ def main():
                     cc = comms_sched
                 else:
                     kw = {**common, "mode": sched, "zero": common["zero"] and sched == "depcha"}
-                    coll = config["collectives"]
+                    coll = path["collectives"]
                     cc = []
                 ms_s = api.SynthModel(engine, transport, rank, world, keys, concom_comms=cc, **kw)
                 ms_s.init()
                 ms_s.run(args.warmup, COMM)
                 barrier()
                 t_s = max_over_ranks(ms_s.run(args.steps, COMM)) / args.steps
-                scheds[sched] = {"value": round(world * gbytes / (t_s * 1e6), 3), "ms_per_step": round(t_s, 4),
+                scheds[sched] = {"value": round(gbytes / (t_s * 1e6), 3), "ms_per_step": round(t_s, 4),
                                  "collectives": coll}
                 ms_s.close()
             line["schedules"] = scheds
@@ -469,12 +607,33 @@ def main():
             model_v.run(args.warmup, COMM)
             barrier()
             ms_v = max_over_ranks(model_v.run(args.steps, COMM)) / args.steps
-            line["grad_views"] = {"value": round(world * gbytes / (ms_v * 1e6), 3), "unit": "GB/s",
+            line["grad_views"] = {"value": round(gbytes / (ms_v * 1e6), 3), "unit": "GB/s",
                                   "ms_per_step": round(ms_v, 4),
                                   "note": "gradients produced in place in the comm buckets (DDP "
                                           "gradient_as_bucket_view): push copies nothing; same collective "
                                           "and fused update"}
             model_v.close()
+
+        # ---- the reference's own arithmetic: fp64 weights + gradients, plain SGD
+        if dtype == "fp32" and not concom:
+            kw64 = {**common, "w_dtype": api.F64, "g_dtype": api.F64, "comm_dtype": api.F64, "momentum": 0.0,
+                    "grad_views": False, "backward_ns": 0}
+            m64 = api.SynthModel(engine, transport, rank, world, keys, **kw64)
+            m64.init()
+            m64.run(1, BWD | COMM)
+            m64.run(max(0, args.warmup - 1), COMM)
+            barrier()
+            t64 = max_over_ranks(m64.run(args.steps, COMM)) / args.steps
+            m64.close()
+            g64 = sum(keys) * 8
+            line["f64"] = {"value": round(g64 / (t64 * 1e6), 3), "unit": "GB/s", "ms_per_step": round(t64, 4),
+                           "value_same_basis_as_headline": round(gbytes / (t64 * 1e6), 3),
+                           "note": "fp64 weights and gradients, plain SGD (momentum 0): the reference's own "
+                                   "arithmetic (model.cpp:17-27), directly comparable to the --impl reference "
+                                   "line; value counts fp64 bytes, value_same_basis_as_headline the headline's"}
+            if args.parity:
+                line["f64"]["parity"] = parity_check(api, engine, transport, rank, world, keys, kw64, [], api.F64,
+                                                     args.parity_steps, barrier, dist)
 
         # ---- end to end through the C ABI with host buffers
         model_e2e = api.SynthModel(engine, transport, rank, world, keys, concom_comms=comms_e2e,
@@ -484,7 +643,7 @@ def main():
         barrier()
         wall = max_over_ranks(model_e2e.run_e2e(args.steps, BWD | COMM))
         e2e_step = wall / args.steps
-        line["e2e"] = {"value": round(world * gbytes / (e2e_step * 1e6), 3), "unit": "GB/s",
+        line["e2e"] = {"value": round(gbytes / (e2e_step * 1e6), 3), "unit": "GB/s",
                        "h2d_bytes_per_step": model_e2e.info()["h2d_bytes_per_step"], "d2h_bytes_per_step": 8,
                        "ms_per_step": round(e2e_step, 4),
                        "note": "wall clock through the C ABI: per step one pinned-host H2D of the gradients, "
@@ -495,17 +654,22 @@ def main():
         # ---- CPU baseline: the reference on this host, bounded sample
         if world == 1 and rank == 0:
             try:
-                ref = run_reference(args, keys, mode, outstanding, 1)
+                ref = run_reference(keys, mode, outstanding, 1, 1, args.cpu_steps, ELEM[dtype])
             except Exception as e:  # reported, not fatal
                 ref = None
                 line["cpu_baseline"] = {"error": str(e)}
             if ref:
                 line["cpu_baseline"] = {
-                    "value": round(ref["per_rank"], 4), "unit": "GB/s", "cores": ref["cores"], "kind": "reference",
+                    "value": round(ref["per_gpu"], 4), "unit": "GB/s", "cores": ref["cores"], "kind": "reference",
                     "sample": f"{len(keys)} keys fp64, 1 rank thread x {ref['threads']} engine threads, "
-                              f"{args.cpu_steps} iterations after 1 warm-up (oracle/_ref = unmodified reference)",
+                              f"{args.cpu_steps} steps after 1 warm-up (oracle/_ref = unmodified reference)",
                     "ms_per_step": round(ref["ms_per_step"], 2)}
     model.close()
+
+    # ---- parity of the benchmarked config (after every timed region)
+    if args.parity:
+        line["parity"] = parity_check(api, engine, transport, rank, world, keys, common, comms_par, dt,
+                                      args.parity_steps, barrier, dist)
     if rank == 0:
         print(json.dumps(line), flush=True)
     barrier()
@@ -513,7 +677,8 @@ def main():
     transport.close()
     if world > 1:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

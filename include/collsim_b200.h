@@ -144,6 +144,13 @@ int cs_engine_new_lane(cs_engine_t e, int priority, int* lane);
 int cs_engine_lane_stream(cs_engine_t e, int lane, cs_stream_t* out);
 int cs_engine_stats(cs_engine_t e, uint64_t* pushed, uint64_t* completed);
 int cs_engine_num_threads(cs_engine_t e, int* out);
+/* Device waits (wait_for / wait_all) give up after `ms` (default 600 s): every
+ * transport is aborted first -- peer kernels leave their pair barriers, NCCL
+ * communicators are aborted, ledgers latch -- then CS_ERR_DEADLOCK is
+ * returned (collective.cpp:249-264 watchdog -> report -> latch).  The same
+ * waits poll for asynchronous failures (ncclCommGetAsyncError, a peer
+ * kernel's device timeout) every ~50 ms. */
+int cs_engine_set_watchdog(cs_engine_t e, int64_t ms);
 
 /* --------------------------------------------------------- transport */
 typedef struct cs_transport* cs_transport_t;
@@ -151,6 +158,12 @@ typedef struct cs_transport* cs_transport_t;
  * arriver reduces with kernel (b) in rank order (collective.cpp:228-236). */
 int cs_transport_create_local(int num_ranks, int watchdog_ms, cs_trace_t trace,
                               cs_transport_t* out);
+/* Same, but the rank threads run the fused peer-memory kernels (the path the
+ * NCCL transport takes across GPUs) directly on each other's buffers: plain
+ * device pointers, every rank's grid capped so all grids are co-resident on
+ * one GPU.  Exercises the cross-GPU kernels, barriers and epochs on one device. */
+int cs_transport_create_local_peer(int num_ranks, int watchdog_ms, cs_trace_t trace,
+                                   cs_transport_t* out);
 /* One process per GPU: matching ledger in POSIX shared memory `name`
  * (rank 0 creates it), data over NCCL (NVLink / NVSwitch). */
 int cs_transport_create_nccl(const char* name, int num_ranks, int rank, int device,
@@ -175,8 +188,17 @@ int cs_barrier(cs_transport_t t, int comm, int rank, int trace_key, cs_stream_t 
  * ptrs_out[r] = rank r's buffer as seen from this process. */
 int cs_transport_p2p_capable(cs_transport_t t, int* out);
 int cs_transport_share_buffer(cs_transport_t t, void* base, void** ptrs_out);
+/* same, naming the calling rank (required by a local peer transport, whose
+ * one object serves every rank thread) */
+int cs_transport_share_buffer_rank(cs_transport_t t, int rank, void* base, void** ptrs_out);
+/* a peer kernel's device timeout (CSB_P2P_TIMEOUT_MS, default 30 s: the pair
+ * barrier records where it waited and the kernel returns -- no __trap) or an
+ * NCCL asynchronous error, as text into buf ("" when healthy) */
+int cs_transport_device_failure(cs_transport_t t, char* buf, int cap);
 /* allreduce of peer_bufs[*] (n elements, multiple of 8) in rank order, every
- * rank ends with the sum; with upd != NULL fused with the SGD / momentum
+ * rank ends with the sum.  Launches of one (comm, rank) run in call order even
+ * on different streams (they share the comm's flag region); every rank must
+ * pass the same update / shard_only choice (else CS_ERR_MISMATCH); with upd != NULL fused with the SGD / momentum
  * update of the listed weights (entries address the bucket by element
  * offset: entry.g = &bucket[offset], offset a multiple of 8). */
 typedef struct cs_p2p_update {
@@ -295,6 +317,9 @@ int cs_synth_run(cs_synth_t s, int steps, int flags, double* device_ms);
 /* host wall time of `steps` steps, each ending with the result on the host */
 int cs_synth_run_e2e(cs_synth_t s, int steps, int flags, double* wall_ms);
 int cs_synth_checksum(cs_synth_t s, double* out);
+/* every key's weights, concatenated without padding, into host memory
+ * (bytes = sum n_k * sizeof(w_dtype)); waits for this rank's work first */
+int cs_synth_read_weights(cs_synth_t s, void* host, uint64_t bytes);
 int cs_synth_info(cs_synth_t s, uint64_t* grad_bytes, uint64_t* h2d_bytes_per_step, int* num_buckets);
 /* host time the last cs_synth_run spent dispatching (enqueue-bound check) */
 int cs_synth_last_host_ms(cs_synth_t s, double* out);

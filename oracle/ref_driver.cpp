@@ -222,15 +222,19 @@ int ref_run_scenario(const char* mode, int workers, int engine_threads, int outs
 }
 
 // CPU bench arm (the reference's own path, timed): R rank threads x T engine
-// threads, K keys of sizes[k] fp64 elements.  Per iteration a synthetic
-// backward pushes one copy op per key (src -> g) in descending key order,
-// chained on one "backward" tag, then the trainer loop of `mode` runs
-// push/pull/sgd (trainer.cpp:112-141).  compute_only=1 runs the backward and
-// the sgd ops without the kvstore (exposed-comm denominator).
+// threads, K keys of sizes[k] fp64 elements, gradients g = random_uniform(n_k,
+// 1000 + rank*K + k) (test_kvstore.cpp:304 seeds).  One iteration is the
+// trainer loop of `mode` (trainer.cpp:112-141): push(g) / pull(out) / sgd
+// (w -= lr*rescale*out) -- the same work the GPU headline step times
+// (push = pack, allreduce, pull + update).  flags:
+//   1  compute only: sgd ops without the kvstore (exposed-comm denominator)
+//   2  also a synthetic backward per iteration: one copy op per key
+//      (src -> g) in descending key order, chained on one "backward" tag
 // stats[0] = mean ms/iter (max over ranks), stats[1] = fp64 grad bytes/iter/rank.
 int ref_bench(const char* mode_name, int R, int T, int outstanding, int K, const int64_t* sizes,
-              int warmup, int iters, int compute_only, double lr, double rescale,
+              int warmup, int iters, int flags, double lr, double rescale,
               double* stats) {
+  const bool compute_only = (flags & 1) != 0, backward = (flags & 2) != 0;
   try {
     Transport transport(R, std::chrono::milliseconds(600000));
     KvMode mode = parse_kv_mode(mode_name);
@@ -239,40 +243,45 @@ int ref_bench(const char* mode_name, int R, int T, int outstanding, int K, const
     int64_t total = 0;
     for (int k = 0; k < K; ++k) total += sizes[k];
     int rc = kv_ranks(R, T, cfg, transport, nullptr, [&](int rank, Engine& engine, KvStore& store) {
-      std::vector<Tensor> w, g, src;
-      std::vector<Tag> wt, gt;
+      std::vector<Tensor> w, g, src, out;
+      std::vector<Tag> wt, gt, ot;
       for (int k = 0; k < K; ++k) {
         w.push_back(random_uniform(Shape{sizes[k]}, mix_seed(7, static_cast<uint64_t>(k))));
-        g.push_back(Tensor(Shape{sizes[k]}));
         src.push_back(random_uniform(Shape{sizes[k]}, 1000 + static_cast<uint64_t>(rank * K + k)));
+        g.push_back(src.back());
+        out.push_back(Tensor(Shape{sizes[k]}));
         wt.push_back(engine.new_variable());
         gt.push_back(engine.new_variable());
+        ot.push_back(engine.new_variable());
       }
       Tag bwd = engine.new_variable();
       if (!compute_only) {
         for (int k = 0; k < K; ++k) store.init(k, TensorSlot{w[k], wt[k]});
       }
       engine.wait_all();
-      auto sgd = [&](int k) {
+      // sgd_update(w, aggregated gradient) as push_sgd_update (trainer.cpp:74-80)
+      auto sgd = [&](int k, bool aggregated) {
         Tensor* wp = &w[k];
-        Tensor* gp = &g[k];
-        engine.push([wp, gp, lr, rescale] { sgd_update(*wp, *gp, lr, rescale); }, {gt[k]},
-                    {wt[k]}, OpKind::Compute, k);
+        Tensor* gp = aggregated ? &out[k] : &g[k];
+        engine.push([wp, gp, lr, rescale] { sgd_update(*wp, *gp, lr, rescale); },
+                    {aggregated ? ot[k] : gt[k]}, {wt[k]}, OpKind::Compute, k);
       };
       auto one_iter = [&] {
-        for (int k = K - 1; k >= 0; --k) {
-          Tensor* gp = &g[k];
-          const Tensor* sp = &src[k];
-          engine.push([gp, sp] { copy(*sp, *gp); }, {}, {gt[k], bwd}, OpKind::Compute, k);
+        if (backward) {
+          for (int k = K - 1; k >= 0; --k) {
+            Tensor* gp = &g[k];
+            const Tensor* sp = &src[k];
+            engine.push([gp, sp] { copy(*sp, *gp); }, {}, {gt[k], bwd}, OpKind::Compute, k);
+          }
         }
         if (compute_only) {
-          for (int k = 0; k < K; ++k) sgd(k);
+          for (int k = 0; k < K; ++k) sgd(k, false);
         } else if (mode == KvMode::Funnel || mode == KvMode::ConCom) {
           int since = 0;
           for (int k = 0; k < K; ++k) {
             store.push(k, TensorSlot{g[k], gt[k]});
-            store.pull(k, TensorSlot{g[k], gt[k]});
-            sgd(k);
+            store.pull(k, TensorSlot{out[k], ot[k]});
+            sgd(k, true);
             if (mode == KvMode::ConCom && ++since == outstanding) {
               store.barrier();
               since = 0;
@@ -282,8 +291,8 @@ int ref_bench(const char* mode_name, int R, int T, int outstanding, int K, const
         } else {
           for (int k = 0; k < K; ++k) store.push(k, TensorSlot{g[k], gt[k]});
           for (int k = 0; k < K; ++k) {
-            store.pull(k, TensorSlot{g[k], gt[k]});
-            sgd(k);
+            store.pull(k, TensorSlot{out[k], ot[k]});
+            sgd(k, true);
           }
         }
         engine.wait_all();

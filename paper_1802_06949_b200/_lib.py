@@ -89,7 +89,9 @@ SIGNATURES = {
     "cs_engine_lane_stream": [_P, _I, C.POINTER(_P)],
     "cs_engine_stats": [_P, _PU64, _PU64],
     "cs_engine_num_threads": [_P, _PI],
+    "cs_engine_set_watchdog": [_P, C.c_int64],
     "cs_transport_create_local": [_I, _I, _P, C.POINTER(_P)],
+    "cs_transport_create_local_peer": [_I, _I, _P, C.POINTER(_P)],
     "cs_transport_create_nccl": [C.c_char_p, _I, _I, _I, _I, _P, C.POINTER(_P)],
     "cs_transport_create_ledger_only": [C.c_char_p, _I, _I, _I, _P, C.POINTER(_P)],
     "cs_transport_destroy": [_P],
@@ -103,6 +105,8 @@ SIGNATURES = {
     "cs_barrier": [_P, _I, _I, _I, _P],
     "cs_transport_p2p_capable": [_P, _PI],
     "cs_transport_share_buffer": [_P, _P, C.POINTER(_P)],
+    "cs_transport_share_buffer_rank": [_P, _I, _P, C.POINTER(_P)],
+    "cs_transport_device_failure": [_P, C.c_char_p, _I],
     "cs_allreduce_p2p": [_P, _I, _I, C.POINTER(_P), _U64, _I, _I, C.c_void_p, _P],
     "cs_transport_nvls_capable": [_P, _PI],
     "cs_transport_alloc_nvls": [_P, _U64, C.POINTER(_P), C.POINTER(_P)],
@@ -131,6 +135,7 @@ SIGNATURES = {
     "cs_synth_run": [_P, _I, _I, C.POINTER(C.c_double)],
     "cs_synth_run_e2e": [_P, _I, _I, C.POINTER(C.c_double)],
     "cs_synth_checksum": [_P, C.POINTER(C.c_double)],
+    "cs_synth_read_weights": [_P, _P, _U64],
     "cs_synth_info": [_P, _PU64, _PU64, _PI],
     "cs_synth_last_host_ms": [_P, C.POINTER(C.c_double)],
     "cs_launch_count": [_PU64],

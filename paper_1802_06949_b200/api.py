@@ -238,6 +238,10 @@ class Engine:
         check(lib.cs_engine_lane_stream(self.h, lane, C.byref(s)))
         return s.value or 0
 
+    def set_watchdog(self, ms: int) -> None:
+        """Device waits give up (DeadlockTimeout, every transport aborted) after ms."""
+        check(lib.cs_engine_set_watchdog(self.h, int(ms)))
+
     def num_threads(self) -> int:
         n = C.c_int()
         check(lib.cs_engine_num_threads(self.h, C.byref(n)))
@@ -282,10 +286,14 @@ class Transport:
         return 0
 
     @classmethod
-    def local(cls, num_ranks: int, watchdog_ms: int = 5000, trace: TraceSink | None = None):
+    def local(cls, num_ranks: int, watchdog_ms: int = 5000, trace: TraceSink | None = None,
+              peer: bool = False):
+        """In-process rank threads.  peer=True: the rank threads run the fused
+        peer-memory kernels on each other's buffers (one GPU; every rank's grid
+        capped so all grids are co-resident) instead of the last-arriver sum."""
         h = C.c_void_p()
-        check(lib.cs_transport_create_local(num_ranks, watchdog_ms, trace.h if trace else None,
-                                            C.byref(h)))
+        fn = lib.cs_transport_create_local_peer if peer else lib.cs_transport_create_local
+        check(fn(num_ranks, watchdog_ms, trace.h if trace else None, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -343,11 +351,22 @@ class Transport:
         check(lib.cs_transport_p2p_capable(self.h, C.byref(v)))
         return bool(v.value)
 
-    def share_buffer(self, base: int) -> list[int]:
+    def share_buffer(self, base: int, rank: int | None = None) -> list[int]:
+        """Setup collective: every rank's mapping of its peers' allocation.
+        rank is required on a local peer transport (one object, many ranks)."""
         n = self.num_ranks()
         out = (C.c_void_p * n)()
-        check(lib.cs_transport_share_buffer(self.h, base, out))
+        if rank is None:
+            check(lib.cs_transport_share_buffer(self.h, base, out))
+        else:
+            check(lib.cs_transport_share_buffer_rank(self.h, rank, base, out))
         return [p or 0 for p in out]
+
+    def device_failure(self) -> str:
+        """A peer kernel's device timeout or an NCCL asynchronous error ("" if none)."""
+        buf = C.create_string_buffer(512)
+        check(lib.cs_transport_device_failure(self.h, buf, 512))
+        return buf.value.decode()
 
     @staticmethod
     def _update_arg(update):
@@ -602,6 +621,8 @@ class SynthModel:
         self.h = h
         self.engine = engine
         self.transport = transport
+        self.sizes = list(sizes)
+        self.w_dtype = w_dtype
 
     def init(self) -> None:
         check(lib.cs_synth_init(self.h))
@@ -623,6 +644,14 @@ class SynthModel:
         v = C.c_double()
         check(lib.cs_synth_checksum(self.h, C.byref(v)))
         return v.value
+
+    def read_weights(self):
+        """Every key's weights (numpy, the weight dtype), keys concatenated."""
+        import numpy as np
+        dt = {F64: np.float64, F32: np.float32, BF16: np.uint16}[self.w_dtype]
+        out = np.empty(int(sum(self.sizes)), dtype=dt)
+        check(lib.cs_synth_read_weights(self.h, out.ctypes.data, out.nbytes))
+        return out
 
     def last_host_ms(self) -> float:
         v = C.c_double()

@@ -275,6 +275,13 @@ int cs_engine_stats(cs_engine_t e, uint64_t* pushed, uint64_t* completed) {
     *completed = e->e->ops_completed();
   });
 }
+int cs_engine_set_watchdog(cs_engine_t e, int64_t ms) {
+  return guard([&] {
+    CHECK_HANDLE(e);
+    if (ms < 1) throw UsageError("Engine: watchdog must be >= 1 ms");
+    e->e->set_watchdog(std::chrono::milliseconds(ms));
+  });
+}
 int cs_engine_num_threads(cs_engine_t e, int* out) {
   return guard([&] {
     CHECK_HANDLE(e);
@@ -288,6 +295,14 @@ int cs_transport_create_local(int num_ranks, int watchdog_ms, cs_trace_t trace, 
     auto h = std::make_unique<cs_transport>();
     h->t = Transport::create_local(num_ranks, std::chrono::milliseconds(watchdog_ms),
                                    trace ? &trace->sink : nullptr);
+    *out = h.release();
+  });
+}
+int cs_transport_create_local_peer(int num_ranks, int watchdog_ms, cs_trace_t trace, cs_transport_t* out) {
+  return guard([&] {
+    auto h = std::make_unique<cs_transport>();
+    h->t = Transport::create_local(num_ranks, std::chrono::milliseconds(watchdog_ms),
+                                   trace ? &trace->sink : nullptr, true);
     *out = h.release();
   });
 }
@@ -376,6 +391,24 @@ int cs_transport_share_buffer(cs_transport_t t, void* base, void** ptrs_out) {
     CHECK_HANDLE(t);
     std::vector<void*> p = t->t->share_buffer(base);
     for (size_t i = 0; i < p.size(); ++i) ptrs_out[i] = p[i];
+  });
+}
+int cs_transport_share_buffer_rank(cs_transport_t t, int rank, void* base, void** ptrs_out) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    std::vector<void*> p = t->t->share_buffer(base, rank);
+    for (size_t i = 0; i < p.size(); ++i) ptrs_out[i] = p[i];
+  });
+}
+int cs_transport_device_failure(cs_transport_t t, char* buf, int cap) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    const std::string m = t->t->async_failure();
+    if (cap > 0) {
+      const size_t n = std::min<size_t>(m.size(), static_cast<size_t>(cap) - 1);
+      std::memcpy(buf, m.data(), n);
+      buf[n] = '\0';
+    }
   });
 }
 namespace {
@@ -687,6 +720,12 @@ int cs_synth_checksum(cs_synth_t s, double* out) {
   return guard([&] {
     CHECK_HANDLE(s);
     *out = s->m->checksum();
+  });
+}
+int cs_synth_read_weights(cs_synth_t s, void* host, uint64_t bytes) {
+  return guard([&] {
+    CHECK_HANDLE(s);
+    s->m->read_weights(host, bytes);
   });
 }
 int cs_synth_info(cs_synth_t s, uint64_t* grad_bytes, uint64_t* h2d, int* num_buckets) {

@@ -5,6 +5,7 @@
 //   worker loop, poison            R/core/src/engine.cpp:163-215
 //   wait_for / wait_all / shutdown R/core/src/engine.cpp:217-246
 #include "engine.hpp"
+#include "watch.hpp"
 
 #include "hostprof.hpp"
 
@@ -311,17 +312,42 @@ EventRef Engine::acquire_event(int lane) {
   return ref;
 }
 
+// Device waits double as the failure detector of device-side collectives
+// (watch.hpp): every ~50 ms of waiting they poll the registered transports
+// (NCCL asynchronous errors, a peer kernel's device timeout); on a failure
+// or on this engine's watchdog every transport is aborted -- peer kernels
+// leave their pair barriers, NCCL communicators are aborted, the ledgers
+// latch -- before the error is thrown, so the device work drains instead of
+// hanging the GPU (collective.cpp:92-105, 249-264: timeout -> report -> latch).
+void Engine::device_wait_tick(std::chrono::steady_clock::time_point deadline,
+                              std::chrono::steady_clock::time_point& next_poll, const char* what) {
+  const auto now = std::chrono::steady_clock::now();
+  if (now >= next_poll) {
+    next_poll = now + std::chrono::milliseconds(50);
+    const std::string m = watch::poll();
+    if (!m.empty()) {
+      watch::abort_all(m);
+      throw DeadlockTimeout("Engine: device collective failed while waiting (" + std::string(what) + "): " + m);
+    }
+  }
+  if (now > deadline) {
+    const std::string m = std::string("Engine: device work not complete after ") +
+                          std::to_string(watchdog_.count()) + " ms (" + what + ")";
+    watch::abort_all(m);
+    throw DeadlockTimeout(m);
+  }
+}
+
 void Engine::sync_event(const EventRef& ev, const char* what) {
   if (!ev) return;
   const auto deadline = std::chrono::steady_clock::now() + watchdog_;
+  auto next_poll = std::chrono::steady_clock::now() + std::chrono::milliseconds(50);
   int spins = 0;
   for (;;) {
     cudaError_t e = cudaEventQuery(ev->ev);
     if (e == cudaSuccess) return;
     if (e != cudaErrorNotReady) throw_cuda(e, what, __FILE__, __LINE__);
-    if (std::chrono::steady_clock::now() > deadline)
-      throw DeadlockTimeout(std::string("Engine: device work not complete after ") +
-                            std::to_string(watchdog_.count()) + " ms (" + what + ")");
+    device_wait_tick(deadline, next_poll, what);
     if (++spins < 64) std::this_thread::yield();
     else std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
@@ -336,15 +362,14 @@ void Engine::sync_lanes() {
     lanes = lanes_;
   }
   const auto deadline = std::chrono::steady_clock::now() + watchdog_;
+  auto next_poll = std::chrono::steady_clock::now() + std::chrono::milliseconds(50);
   for (cudaStream_t s : lanes) {
     int spins = 0;
     for (;;) {
       cudaError_t e = cudaStreamQuery(s);
       if (e == cudaSuccess) break;
       if (e != cudaErrorNotReady) throw_cuda(e, "cudaStreamQuery", __FILE__, __LINE__);
-      if (std::chrono::steady_clock::now() > deadline)
-        throw DeadlockTimeout("Engine: lane work not complete after " +
-                              std::to_string(watchdog_.count()) + " ms");
+      device_wait_tick(deadline, next_poll, "lane work");
       if (++spins < 64) std::this_thread::yield();
       else std::this_thread::sleep_for(std::chrono::microseconds(20));
     }

@@ -110,6 +110,7 @@ class Engine {
   uint64_t ops_pushed() const;
   uint64_t ops_completed() const;
   void set_watchdog(std::chrono::milliseconds ms) { watchdog_ = ms; }
+  std::chrono::milliseconds watchdog() const { return watchdog_; }
   TraceSink* trace() const { return trace_; }
 
   // Makes the calling thread's current device the engine's device.
@@ -154,6 +155,8 @@ class Engine {
   EventRef acquire_event(int lane);
   void sync_event(const EventRef& ev, const char* what);
   void sync_lanes();
+  void device_wait_tick(std::chrono::steady_clock::time_point deadline,
+                        std::chrono::steady_clock::time_point& next_poll, const char* what);
 
   const uint64_t engine_id_;
   const int rank_;

@@ -573,6 +573,8 @@ struct P2PParams {
   void* wm[CS_MAX_RANKS];    // ZeRO-1: every rank's master-weight shard (shard-local layout)
   void* mom_b;               // ZeRO-1: this rank's momentum shard (shard-local layout)
   const DevEntry* tab;
+  uint32_t* abort_word;      // host-mapped: [0] abort code, [1..3] rank / phase / CTA of a timeout
+  uint64_t timeout_ns;
   uint64_t groups;
   double step, mu;
   int nranks, rank, n_entries, shard_only;
@@ -588,10 +590,28 @@ __device__ __forceinline__ uint32_t flag_load(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t abort_load(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // phase: 0 = arrival (my bucket is packed), 1 = my shard sums are stored,
-// 2 = (shard_only) my update finished reading the owners' buckets
-__device__ __forceinline__ void pair_barrier(const P2PParams& p, int phase) {
+// 2 = (shard_only) my update finished reading the owners' buckets.
+// Returns false when the launch was aborted: the host set the abort word
+// (engine watchdog, Transport::abort, a failed peer), or this CTA waited
+// longer than timeout_ns for a peer and recorded kAbortDeviceTimeout.  The
+// caller then returns at once -- the GPU stays usable (no __trap), and the
+// host reports DeadlockTimeout.  The abort word lives in host memory, so it
+// is read only after the first ~20 us of waiting, then every ~20 us.
+__device__ __forceinline__ bool pair_barrier(const P2PParams& p, int phase) {
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = 0;
   __syncthreads();
   const int t = threadIdx.x;
   if (t < p.nranks) {
@@ -603,15 +623,36 @@ __device__ __forceinline__ void pair_barrier(const P2PParams& p, int phase) {
     flag_store(p.flags[t] + slot, p.epoch);
     const uint32_t* mine =
         p.flags[p.rank] + (static_cast<size_t>(phase) * CS_MAX_RANKS + t) * kP2PMaxCtas + blockIdx.x;
-    uint64_t t0, now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint64_t t0 = 0, next_poll = 0;
     while (static_cast<int32_t>(flag_load(mine) - p.epoch) < 0) {
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 60000000000ull) __trap();  // a peer never arrived: fail loudly, never hang
-      __nanosleep(100);
+      const uint64_t now = now_ns();
+      if (t0 == 0) {
+        t0 = now;
+        next_poll = now + 20000;
+      } else if (now >= next_poll) {
+        next_poll = now + 20000;
+        if (p.abort_word && abort_load(p.abort_word) != 0) {
+          s_abort = 1;
+          break;
+        }
+        if (now - t0 > p.timeout_ns) {
+          if (p.abort_word) {
+            // where: rank, phase, CTA and the peer that never arrived
+            p.abort_word[1] = static_cast<uint32_t>(p.rank);
+            p.abort_word[2] = static_cast<uint32_t>(phase) | (static_cast<uint32_t>(t) << 8);
+            p.abort_word[3] = blockIdx.x;
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.abort_word), "r"(2u) : "memory");
+          }
+          s_abort = 1;
+          break;
+        }
+      }
+      __nanosleep(64);
     }
   }
   __syncthreads();
+  return s_abort == 0;
 }
 
 template <int CDT, int M>
@@ -734,7 +775,7 @@ template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
   const uint64_t T = p.groups;
   const uint64_t G = gridDim.x, c = blockIdx.x;
-  pair_barrier(p, 0);
+  if (!pair_barrier(p, 0)) return;
   {
     const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
     if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
@@ -750,7 +791,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __g
     __syncthreads();
     update_shard(p.rank);
   }
-  pair_barrier(p, 1);
+  if (!pair_barrier(p, 1)) return;
   if constexpr (UPDATE) {
     // the other shards, staggered so the ranks start on different owners
     for (int k = NVLS ? 0 : 1; k < p.nranks; ++k) update_shard((p.rank + k) % p.nranks);
@@ -861,12 +902,12 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_c
     b = s0 + L * (c + 1) / G;
   };
   uint64_t s0, a, b;
-  pair_barrier(p, 0);
+  if (!pair_barrier(p, 0)) return;
   chunk(p.rank, s0, a, b);
   zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b);
   __syncthreads();
   zero_gather<WDT>(p, p.rank, s0, a, b);  // own shard: no need to wait for the peers
-  pair_barrier(p, 1);
+  if (!pair_barrier(p, 1)) return;
   for (int k = 1; k < p.nranks; ++k) {
     const int s = (p.rank + k) % p.nranks;
     chunk(s, s0, a, b);
@@ -1420,16 +1461,33 @@ uint64_t p2p_shard_elems(uint64_t count, int nranks) {
 }
 
 // The grid is a pure function of (groups, nranks): identical on every rank,
-// as the per-CTA pairing requires; <= 2 CTAs per SM so the cooperative launch
-// fits beside the other lanes' kernels.
-int p2p_grid(uint64_t groups, int nranks) {
+// as the per-CTA pairing requires; one 512-thread CTA per SM so the
+// cooperative launch fits beside the other lanes' kernels.  Colocated ranks
+// (every rank's grid on one device, local peer transport) share the SMs:
+// each grid gets at most 1/nranks of the device's resident 512-thread CTAs,
+// so all nranks grids are resident at once and the pair barriers can meet.
+int p2p_grid(uint64_t groups, int nranks, bool colocated) {
   static const uint64_t cap = [] {
     const char* e = std::getenv("CSB_P2P_CTAS");  // identical on every rank (same environment)
     return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 148);
   }();
+  uint64_t limit = std::min<uint64_t>(cap, kP2PMaxCtas);
+  if (colocated) {
+    const uint64_t resident = static_cast<uint64_t>(sm_count_for_current_device()) * 2;  // __launch_bounds__(512, 2)
+    limit = std::min<uint64_t>(limit, std::max<uint64_t>(1, resident / static_cast<uint64_t>(nranks)));
+  }
   const uint64_t per_rank = groups / static_cast<uint64_t>(nranks);
   const uint64_t want = std::max<uint64_t>(1, per_rank / (2 * kP2PLinkThreads));
-  return static_cast<int>(std::min<uint64_t>(std::min<uint64_t>(want, cap), kP2PMaxCtas));
+  return static_cast<int>(std::min<uint64_t>(want, limit));
+}
+
+uint64_t p2p_timeout_ns() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("CSB_P2P_TIMEOUT_MS");
+    const long long ms = e ? std::atoll(e) : 30000;
+    return static_cast<uint64_t>(std::max<long long>(1, ms)) * 1000000ull;
+  }();
+  return v;
 }
 
 void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
@@ -1459,7 +1517,9 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     if (!aligned16(a.wm[r])) throw UsageError("p2p_allreduce: master shard not 16-byte aligned");
   }
   p.mom_b = a.mom_b;
-  const int grid = p2p_grid(p.groups, a.nranks);
+  p.abort_word = a.abort_word;
+  p.timeout_ns = a.timeout_ns ? a.timeout_ns : p2p_timeout_ns();
+  const int grid = p2p_grid(p.groups, a.nranks, a.colocated);
   const bool upd = a.update && a.tab && a.n_entries > 0;
   const bool mom = a.momentum != 0.0;
   const double elems = static_cast<double>(a.count);
@@ -1531,7 +1591,9 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     return (e && std::string(e) == "1") ? 1 : 0;
   }();
   p.sys_fence = fence;
-  if (coop) CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
+  // colocated grids share one device: a cooperative launch would claim the
+  // whole device per grid, so those launch plainly (p2p_grid keeps them co-resident)
+  if (coop && !a.colocated) CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   else CSB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   ls.done();
 }

@@ -81,12 +81,25 @@ struct P2PArgs {
   void* wm[CS_MAX_RANKS] = {};
   void* mom_b = nullptr;
   double lr = 0, rescale = 0, momentum = 0;
+  // every rank's grid on the SAME device (local peer transport): cap each
+  // grid so all `nranks` grids are co-resident, plain (non-cooperative) launch
+  bool colocated = false;
+  // host-mapped abort word (device address): [0] code, [1..3] where.  The
+  // pair barriers poll it while waiting and give up (no __trap) once it is
+  // set, or set it themselves after `timeout_ns` without the peer.
+  uint32_t* abort_word = nullptr;
+  uint64_t timeout_ns = 0;
 };
+// Abort codes in abort_word[0]
+enum : uint32_t { kAbortNone = 0, kAbortHost = 1, kAbortDeviceTimeout = 2 };
 size_t p2p_flag_bytes();
 // elements of the largest shard of a `count`-element bucket (a multiple of 8)
 uint64_t p2p_shard_elems(uint64_t count, int nranks);
-int p2p_grid(uint64_t groups, int nranks);
+int p2p_grid(uint64_t groups, int nranks, bool colocated = false);
 void p2p_allreduce(const P2PArgs& args, cudaStream_t s);
+// CSB_P2P_TIMEOUT_MS (default 30000): a pair barrier waiting longer than this
+// for a peer CTA records kAbortDeviceTimeout and the kernel returns
+uint64_t p2p_timeout_ns();
 
 // Launch accounting and optional per-launch CUDA-event timing (roofline).
 enum KernelKind { kKernPack = 0, kKernSum = 1, kKernSgd = 2, kKernSynth = 3, kKernChecksum = 4, kKernKinds = 5 };

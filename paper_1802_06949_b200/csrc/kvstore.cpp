@@ -302,7 +302,7 @@ void KvStore::build_buckets() {
     }
   } else if (p2p_active_) {
     // setup-phase collective: every rank maps every peer's arena (CUDA IPC)
-    const std::vector<void*> peers = transport_.share_buffer(arena);
+    const std::vector<void*> peers = transport_.share_buffer(arena, rank_);
     shared_.push_back(peers);
     for (Bucket& b : bs) {
       const uint64_t boff = static_cast<uint64_t>(static_cast<char*>(b.base) - arena);
@@ -323,7 +323,7 @@ void KvStore::build_buckets() {
     void* mom = device_alloc_zeroed(shard_total * ms);
     allocations_.push_back(master);
     allocations_.push_back(mom);
-    const std::vector<void*> peers = transport_.share_buffer(master);
+    const std::vector<void*> peers = transport_.share_buffer(master, rank_);
     shared_.push_back(peers);
     uint64_t soff = 0;
     for (Bucket& b : bs) {
@@ -411,6 +411,18 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
     muts.push_back(funnel_tag_);
     engine_.push_stream([self, b](cudaStream_t s) { self->collective_body(self->buckets_[b], b, s, nullptr); },
                         {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+    // The funnel: ONE thread performs every collective, synchronously.  The
+    // reference's push waits for the gradient and runs the allreduce on the
+    // calling (control) thread (kvstore.cpp:112-116), so nothing after it --
+    // the next key, the next iteration's forward -- is issued before the
+    // collective is done.  Same here: the control thread waits until this
+    // bucket's collective has completed on the device.  (CSB_FUNNEL_ASYNC=1
+    // only enqueues it, the stream order alone keeping the funnel order.)
+    static const bool async = [] {
+      const char* e = std::getenv("CSB_FUNNEL_ASYNC");
+      return e && std::string(e) == "1";
+    }();
+    if (!async) engine_.wait_for(B.tag);
   } else {
     // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136)
     std::atomic<int>* outstanding = &outstanding_;
@@ -472,7 +484,9 @@ void KvStore::ensure_momentum(int key, int wdt) {
   const size_t es = (wdt == CS_F64) ? 8 : 4;
   CSB_CUDA(cudaMalloc(&ks.mom, std::max<size_t>(ks.numel * es, 256)));
   CSB_CUDA(cudaMemset(ks.mom, 0, std::max<size_t>(ks.numel * es, 256)));
-  CSB_CUDA(cudaDeviceSynchronize());  // one-time: zeroed before any lane touches it
+  // one-time: zeroed before any lane touches it (the legacy stream only: a
+  // device-wide sync would wait on colocated ranks' peer kernels)
+  CSB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
 }
 
 void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSlot>& outs,
@@ -536,6 +550,13 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       // modelled as a write (the reference holds only a read grant there) --
       // and carries the dummy tag, so collectives stay chained in push order;
       // the copy-out / update follows as an op on the update lane.
+      // this op updates every key of the bucket, so nothing reads the
+      // bucket afterwards: keep only the own shard of the sum locally.
+      // Validated before any bucket / key state changes (a rejected call
+      // leaves the bucket as it was).
+      const bool whole = B.pulled == 0 && idxs.size() == B.keys.size();
+      if (p2p_active_ && upd && zero_active_ && (!whole || out_dt != zero_wdt_))
+        throw UsageError("KvStore: ZeRO-1 needs pull_update of whole fusion buckets into the init weights' dtype");
       std::vector<Tag> muts{B.tag};
       for (const Tag& t : B.view_tags) muts.push_back(t);  // rewritten in place
       if (cfg_.mode == KvMode::DepCha) muts.push_back(dummy_tag_);
@@ -558,11 +579,6 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
         DeviceTable* ptab = B.p2p_tab.get();  // all its uploads on B.lane
         for (const Tag& t : out_tags) muts.push_back(t);
-        // this op updates every key of the bucket, so nothing reads the
-        // bucket afterwards: keep only the own shard of the sum locally
-        const bool whole = B.pulled == 0 && idxs.size() == B.keys.size();
-        if (zero_active_ && (!whole || out_dt != zero_wdt_))
-          throw UsageError("KvStore: ZeRO-1 needs pull_update of whole fusion buckets into the init weights' dtype");
         const bool zero = zero_active_;
         engine_.push_stream(
             [self, bi, es, ptab, out_dt, opt, whole, zero](cudaStream_t s) {

@@ -40,7 +40,14 @@ std::string describe_call(const CallSig& sig) {
   std::ostringstream os;
   os << coll_kind_name(sig.kind);
   if (sig.kind == CollKind::AllreduceSum) {
-    os << "(count=" << sig.count << ")";
+    os << "(count=" << sig.count;
+    if (sig.variant & kVarP2P) {
+      os << ", " << ((sig.variant & kVarNvls) ? "nvls" : "p2p");
+      if (sig.variant & kVarUpdate) os << "+update";
+      if (sig.variant & kVarShardOnly) os << "+shard_only";
+      if (sig.variant & kVarZero) os << "+zero";
+    }
+    os << ")";
   } else if (sig.kind == CollKind::Broadcast) {
     os << "(count=" << sig.count << ", root=" << sig.root << ")";
   }

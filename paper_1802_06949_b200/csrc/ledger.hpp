@@ -38,9 +38,21 @@ struct CallSig {
   int32_t dtype = -1;
   int64_t count = 0;
   int32_t root = -1;
+  // B200 extension: peer-memory kernels pair CTAs across ranks, so every rank
+  // must launch the same barrier protocol (CallVariant bits); 0 = plain call
+  int32_t variant = 0;
   bool operator==(const CallSig& o) const {
-    return kind == o.kind && count == o.count && root == o.root && dtype == o.dtype;
+    return kind == o.kind && count == o.count && root == o.root && dtype == o.dtype && variant == o.variant;
   }
+};
+
+// CallSig::variant bits of a peer-memory allreduce (kernels.cu p2p kernels)
+enum CallVariant : int32_t {
+  kVarP2P = 1,        // fused peer-memory kernel (pair barriers)
+  kVarUpdate = 2,     // fused SGD / momentum update
+  kVarShardOnly = 4,  // update reads the owners' shards; trailing barrier
+  kVarZero = 8,       // ZeRO-1 form
+  kVarNvls = 16,      // NVSwitch multicast reduction
 };
 
 std::string describe_call(const CallSig& sig);

@@ -262,7 +262,7 @@ void SynthModel::enqueue_step(int flags) {
         CSB_CUDA(cudaMemset(p, 0, round_up(cfg_.sizes[k] * es, kAlign)));
         mom_local_.push_back(p);
       }
-      CSB_CUDA(cudaDeviceSynchronize());
+      CSB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
     std::vector<cs_update_entry> es;
     std::vector<Tag> r, m;
@@ -391,6 +391,20 @@ double SynthModel::run_e2e(int steps, int flags) {
   const auto t1 = std::chrono::steady_clock::now();
   engine_.wait_all();
   return std::chrono::duration<double, std::milli>(t1 - t0).count();
+}
+
+void SynthModel::read_weights(void* host, uint64_t bytes) {
+  const uint64_t ws = dtype_size(cfg_.wdt);
+  uint64_t need = 0;
+  for (uint64_t n : cfg_.sizes) need += n * ws;
+  if (bytes != need) throw UsageError("synth: read_weights buffer size differs from the weights' bytes");
+  engine_.wait_all();
+  engine_.bind_device();
+  char* out = static_cast<char*>(host);
+  for (size_t k = 0; k < cfg_.sizes.size(); ++k) {
+    CSB_CUDA(cudaMemcpy(out, w_[k], cfg_.sizes[k] * ws, cudaMemcpyDeviceToHost));
+    out += cfg_.sizes[k] * ws;
+  }
 }
 
 double SynthModel::checksum() {

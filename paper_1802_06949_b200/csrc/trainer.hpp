@@ -66,6 +66,9 @@ class SynthModel {
   // Wall-clock of `steps` steps, each ending with the host reading the result.
   double run_e2e(int steps, int flags);
   double checksum();
+  // Every key's weights, concatenated without padding, into host memory
+  // (bytes = sum n_k * sizeof(wdt)); waits for this rank's work first.
+  void read_weights(void* host, uint64_t bytes);
   // host time the last run() spent enqueueing (dispatching every op)
   double last_host_ms() const { return last_host_ms_; }
   uint64_t grad_bytes() const;

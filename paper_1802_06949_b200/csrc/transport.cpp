@@ -2,9 +2,13 @@
 #include "transport.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
 
 #include "hostprof.hpp"
 #include "kernels.hpp"
+#include "watch.hpp"
 
 namespace csb {
 
@@ -74,11 +78,14 @@ struct Transport::SlotDev {
 };
 
 std::unique_ptr<Transport> Transport::create_local(int nranks, std::chrono::milliseconds watchdog,
-                                                   TraceSink* trace) {
+                                                   TraceSink* trace, bool peer) {
   std::unique_ptr<Transport> t(new Transport());
   t->backend_ = Backend::Local;
   t->ledger_ = Ledger::create_local(nranks, watchdog, trace);
   t->slots_.resize(static_cast<size_t>(kLedgerMaxComms) * kLedgerSlots);
+  t->local_peer_ = peer;
+  t->local_share_next_.assign(static_cast<size_t>(nranks), 0);
+  if (peer) t->setup_abort();
   return t;
 }
 
@@ -141,11 +148,69 @@ std::unique_ptr<Transport> Transport::create_nccl(const std::string& name, int n
     t->name_ = name;
     if (ok) t->setup_flags();
   }
+  t->setup_abort();
   return t;
 }
 
-std::vector<void*> Transport::share_buffer(void* base) {
+// Host-mapped abort word of the peer kernels + registration with the
+// process-wide watch (watch.hpp): the Engine's device waits poll it for
+// asynchronous failures and abort every transport on a timeout.
+void Transport::setup_abort() {
+  CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&abort_host_), 4 * sizeof(uint32_t),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(abort_host_, 0, 4 * sizeof(uint32_t));
+  CSB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&abort_dev_), abort_host_, 0));
+  watch_id_ = watch::add([this] { return async_failure(); }, [this](const std::string& why) { abort(why); });
+}
+
+std::string Transport::device_failure() const {
+  if (!abort_host_) return {};
+  const uint32_t code = reinterpret_cast<volatile uint32_t*>(abort_host_)[0];
+  if (code != kAbortDeviceTimeout) return {};
+  const volatile uint32_t* w = abort_host_;
+  return "peer-memory kernel: rank " + std::to_string(w[1]) + " CTA " + std::to_string(w[3]) +
+         " waited more than " + std::to_string(p2p_timeout_ns() / 1000000) + " ms at pair barrier phase " +
+         std::to_string(w[2] & 0xff) + " for rank " + std::to_string(w[2] >> 8) +
+         " (the peer never launched its half of the collective)";
+}
+
+std::string Transport::async_failure() {
+  std::string m = device_failure();
+  if (!m.empty()) return m;
+  if (backend_ != Backend::Nccl) return {};
+  std::lock_guard<std::mutex> lock(mu_);
+  for (ncclComm_t c : comms_) {
+    if (!c) continue;
+    ncclResult_t r = ncclSuccess;
+    if (ncclCommGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+      return std::string("NCCL asynchronous error: ") + ncclGetErrorString(r);
+  }
+  return {};
+}
+
+std::vector<void*> Transport::share_buffer(void* base, int rank) {
   if (!p2p_capable()) throw UsageError("Transport: peer-memory path needs the NCCL backend on peer-capable GPUs");
+  if (backend_ == Backend::Local) {
+    // rank threads of one process: exchange plain device pointers through
+    // the ledger's per-rank mailbox (same call order on every rank thread)
+    if (rank < 0 || rank >= num_ranks()) throw UsageError("Transport: share_buffer needs the caller's rank");
+    int slot;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      slot = local_share_next_[static_cast<size_t>(rank)]++;
+    }
+    if (slot >= kLedgerRankBlobSlots) throw ConfigError("Transport: too many shared buffers");
+    const uint64_t mine = reinterpret_cast<uintptr_t>(base);
+    ledger_->post_rank_blob(slot, rank, &mine, sizeof(mine));
+    std::vector<void*> ptrs(static_cast<size_t>(num_ranks()), nullptr);
+    for (int r = 0; r < num_ranks(); ++r) {
+      uint64_t v = 0;
+      ledger_->read_rank_blob(slot, r, &v, sizeof(v));
+      ptrs[static_cast<size_t>(r)] = reinterpret_cast<void*>(static_cast<uintptr_t>(v));
+    }
+    return ptrs;
+  }
+  if (rank >= 0 && rank != rank_) throw UsageError("Transport: share_buffer rank differs from this process's rank");
   std::lock_guard<std::mutex> lock(mu_);
   if (share_slots_ >= kLedgerRankBlobSlots - 1) throw ConfigError("Transport: too many shared buffers");
   const int slot = share_slots_++;
@@ -171,6 +236,7 @@ std::vector<void*> Transport::share_buffer(void* base) {
 }
 
 void Transport::unshare_buffer(const std::vector<void*>& ptrs) {
+  if (backend_ != Backend::Nccl) return;  // local peers are plain pointers
   std::lock_guard<std::mutex> lock(mu_);
   cudaSetDevice(device_);
   for (size_t r = 0; r < ptrs.size(); ++r) {
@@ -207,15 +273,72 @@ void Transport::setup_flags() {
   flags_.push_back(share_buffer(f));
 }
 
+// Local peer mode: one flag region per rank thread for `comm`, on the
+// calling rank's device, zeroed on a private stream (no device-wide sync:
+// other ranks' kernels may already be running).
+void Transport::ensure_local_flags(int comm) {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (comm < 0 || comm >= kLedgerMaxComms) throw UsageError("collective: unknown communicator");
+  if (static_cast<int>(flags_.size()) <= comm) flags_.resize(static_cast<size_t>(comm) + 1);
+  auto& f = flags_[static_cast<size_t>(comm)];
+  if (!f.empty()) return;
+  const int R = num_ranks();
+  const size_t bytes = p2p_flag_bytes();
+  char* base = nullptr;
+  CSB_CUDA(cudaMalloc(&base, bytes * static_cast<size_t>(R)));
+  cudaStream_t z;
+  CSB_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
+  CSB_CUDA(cudaMemsetAsync(base, 0, bytes * static_cast<size_t>(R), z));
+  CSB_CUDA(cudaStreamSynchronize(z));
+  CSB_CUDA(cudaStreamDestroy(z));
+  CSB_CUDA(cudaGetDevice(&flags_device_));
+  own_flags_.push_back(base);
+  for (int r = 0; r < R; ++r) f.push_back(base + bytes * static_cast<size_t>(r));
+}
+
+// Peer kernels of one (communicator, rank) share a flag region, so they must
+// run one after another: a launch on a different stream than the previous
+// one first waits for it (the KvStore uses one ordered lane anyway).
+void Transport::serialize_launch(int comm, int rank, cudaStream_t s, bool after) {
+  std::lock_guard<std::mutex> lock(mu_);
+  const size_t idx = static_cast<size_t>(comm) * kLedgerMaxRanks + static_cast<size_t>(rank);
+  if (launch_order_.size() <= idx) launch_order_.resize(static_cast<size_t>(kLedgerMaxComms) * kLedgerMaxRanks);
+  LaunchOrder& lo = launch_order_[idx];
+  if (!after) {
+    if (lo.ev && lo.stream != s) CSB_CUDA(cudaStreamWaitEvent(s, lo.ev, 0));
+    return;
+  }
+  if (!lo.ev) {
+    CSB_CUDA(cudaGetDevice(&lo.dev));
+    CSB_CUDA(cudaEventCreateWithFlags(&lo.ev, cudaEventDisableTiming));
+  }
+  CSB_CUDA(cudaEventRecord(lo.ev, s));
+  lo.stream = s;
+}
+
 void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
                               int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
                               void* mc) {
   if (!p2p_capable()) throw UsageError("Transport: peer-memory path unavailable");
   if (count == 0) throw UsageError("allreduce_sum: empty buffer");
+  if (rank < 0 || rank >= num_ranks()) throw UsageError("collective: rank out of range");
+  if (abort_host_ && reinterpret_cast<volatile uint32_t*>(abort_host_)[0] != kAbortNone) {
+    // a previous peer launch timed out or the transport was aborted: latch
+    const std::string m = device_failure();
+    ledger_->abort(m.empty() ? "Transport: aborted" : m);
+    throw DeadlockTimeout(m.empty() ? "Transport: aborted (peer-memory collectives disabled)" : m);
+  }
+  if (backend_ == Backend::Local) ensure_local_flags(comm);
+  // a launch with no update entries is a plain reduce (kernel without phase 2)
+  if (upd && (!upd->tab || upd->n_entries == 0)) upd = nullptr;
   CallSig sig;
   sig.kind = CollKind::AllreduceSum;
   sig.dtype = dtype;
   sig.count = static_cast<int64_t>(count);
+  // every rank must run the same barrier protocol (a shard_only
+  // rank would wait at a phase-2 barrier its peers never reach)
+  sig.variant = kVarP2P | (mc ? kVarNvls : 0) | (upd ? kVarUpdate : 0) |
+                (upd && upd->shard_only && !mc ? kVarShardOnly : 0) | (upd && upd->wm ? kVarZero : 0);
   Ledger::Ticket t;
   {
     hostprof::Scope prof(hostprof::kLedger);
@@ -234,6 +357,8 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   a.mc = mc;
   a.nranks = num_ranks();
   a.rank = rank;
+  a.colocated = colocated();
+  a.abort_word = abort_dev_;
   a.count = count;
   a.cdt = dtype;
   a.epoch = static_cast<uint32_t>(t.seq + 1);  // same matched sequence on every rank
@@ -253,11 +378,54 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     }
   }
   device_latency(stream);
+  serialize_launch(comm, rank, stream, false);
   p2p_allreduce(a, stream);
+  serialize_launch(comm, rank, stream, true);
   ledger_->depart(t, trace_key, bucket);
+  if (colocated()) wait_colocated(comm, rank);
+}
+
+// Colocated ranks share one device, so their streams share its hardware
+// work queues (CUDA_DEVICE_MAX_CONNECTIONS).  A queue entry that waits on
+// this kernel's completion, submitted after it, could then sit in front of
+// a peer's launch of the same collective in a shared queue -- a false
+// dependency that deadlocks the pair barriers.  So a colocated rank returns
+// only once its peer kernel has completed: nothing it submits afterwards
+// waits on an unfinished peer kernel, and every entry queued ahead of a
+// launch depends only on that rank's own, finite work.
+void Transport::wait_colocated(int comm, int rank) {
+  cudaEvent_t ev;
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    ev = launch_order_[static_cast<size_t>(comm) * kLedgerMaxRanks + static_cast<size_t>(rank)].ev;
+  }
+  int spins = 0;
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) CSB_CUDA(e);
+    if (++spins < 256) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  if (reinterpret_cast<volatile uint32_t*>(abort_host_)[0] != kAbortNone) {
+    const std::string m = device_failure();
+    ledger_->abort(m.empty() ? "Transport: aborted" : m);
+    throw DeadlockTimeout(m.empty() ? "Transport: peer-memory collective aborted while waiting for a peer" : m);
+  }
 }
 
 Transport::~Transport() {
+  if (watch_id_ >= 0) watch::remove(watch_id_);
+  for (LaunchOrder& lo : launch_order_)
+    if (lo.ev) {
+      cudaSetDevice(lo.dev);
+      cudaEventDestroy(lo.ev);
+    }
+  if (backend_ == Backend::Local && !own_flags_.empty()) {
+    cudaSetDevice(flags_device_);
+    for (void* p : own_flags_) cudaFree(p);
+  }
+  if (abort_host_) cudaFreeHost(abort_host_);
   if (backend_ == Backend::Nccl) {
     const bool aborted = ledger_ && ledger_->latched();
     cudaSetDevice(device_);
@@ -277,17 +445,33 @@ int Transport::new_communicator() {
     std::lock_guard<std::mutex> lock(mu_);
     CSB_CUDA(cudaSetDevice(device_));
     ncclComm_t c = nullptr;
-    CSB_NCCL(ncclCommSplit(comms_[0], 0, rank_, &c, nullptr), comms_[0]);
+    // ConCom's communicators run concurrently on one GPU: cap each one's
+    // CTAs so all of them stay resident together (a communicator whose
+    // channels cannot all be scheduled would wait on peers that wait on it)
+    static const int max_ctas = [] {
+      const char* e = std::getenv("CSB_CONCOM_MAX_CTAS");
+      return std::max(1, e ? std::atoi(e) : 16);
+    }();
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.maxCTAs = max_ctas;
+    cfg.minCTAs = std::min(cfg.maxCTAs, 4);
+    CSB_NCCL(ncclCommSplit(comms_[0], 0, rank_, &c, &cfg), comms_[0]);
     if (static_cast<int>(comms_.size()) != id) throw UsageError("Transport: communicator ids diverged");
     comms_.push_back(c);
   }
-  if (p2p_capable()) setup_flags();  // every comm gets its own flag region
+  if (backend_ == Backend::Nccl && p2p_capable()) setup_flags();  // every comm gets its own flag region
   return id;
 }
 
 void Transport::set_inject_latency(std::chrono::microseconds us) { ledger_->set_inject_latency(us); }
 
 void Transport::abort(const std::string& why) {
+  // release every peer kernel still waiting in a pair barrier (they poll
+  // the host-mapped word and return), then latch and abort NCCL
+  if (abort_host_) {
+    volatile uint32_t* w = abort_host_;
+    if (w[0] == kAbortNone) w[0] = kAbortHost;
+  }
   ledger_->abort(why);
   if (backend_ == Backend::Nccl) {
     std::lock_guard<std::mutex> lock(mu_);

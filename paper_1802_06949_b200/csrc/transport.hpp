@@ -12,7 +12,12 @@
 //                   writing the sum to every buffer -- the reference's
 //                   "last arriver reduces" (collective.cpp:228-243) on HBM,
 //                   bit-identical to it.  The others make their stream wait
-//                   on the reducer's done event.
+//                   on the reducer's done event.  With `peer` (create_local
+//                   (..., true)) the rank threads instead run the fused
+//                   peer-memory kernels on each other's buffers (plain device
+//                   pointers, every rank's grid capped so all R grids are
+//                   co-resident on one GPU): the same kernels, barriers and
+//                   epochs as across GPUs, testable on one device.
 //   Backend::Nccl   one process per GPU; ledger in POSIX shm; data over NCCL
 //                   (NVLink 5 / NVSwitch).  One ncclComm_t per communicator
 //                   (world + ConCom's extra communicators, ncclCommSplit).
@@ -39,7 +44,7 @@ class Transport {
   enum class Backend { Local, Nccl, LedgerOnly };
 
   static std::unique_ptr<Transport> create_local(int nranks, std::chrono::milliseconds watchdog,
-                                                 TraceSink* trace);
+                                                 TraceSink* trace, bool peer = false);
   static std::unique_ptr<Transport> create_nccl(const std::string& name, int nranks, int rank,
                                                 int device, std::chrono::milliseconds watchdog,
                                                 TraceSink* trace);
@@ -67,16 +72,28 @@ class Transport {
   Ledger& ledger() { return *ledger_; }
 
   // ---- peer-memory path (one process per GPU, NVLink) --------------------
-  // True for the NCCL backend with >= 2 ranks on peer-capable devices.
-  bool p2p_capable() const { return backend_ == Backend::Nccl && num_ranks() > 1 && p2p_ok_; }
+  // True for the NCCL backend with >= 2 ranks on peer-capable devices, and
+  // for a local transport created with `peer` (>= 2 rank threads).
+  bool p2p_capable() const {
+    return num_ranks() > 1 && ((backend_ == Backend::Nccl && p2p_ok_) || (backend_ == Backend::Local && local_peer_));
+  }
+  bool colocated() const { return backend_ == Backend::Local; }
   // Setup-phase collective: every rank passes the base of one cudaMalloc
   // allocation, in the same order; returns every rank's mapping of its peer
-  // (CUDA IPC handles exchanged through the ledger), own entry = base.
-  std::vector<void*> share_buffer(void* base);
+  // (CUDA IPC handles exchanged through the ledger; local peer mode: the
+  // rank threads' pointers), own entry = base.  `rank` is required for the
+  // local transport (one object serves every rank thread).
+  std::vector<void*> share_buffer(void* base, int rank = -1);
   // Closes this rank's mappings of the peers' buffers returned by
   // share_buffer (before the owner of `ptrs` frees its own buffer, so the
   // same addresses can be shared again later).
   void unshare_buffer(const std::vector<void*>& ptrs);
+  // Device abort word of the peer kernels (host-mapped): 0 while healthy;
+  // set by abort() / the engine watchdog, or by a kernel whose pair barrier
+  // timed out.  Returns the failure description when one was recorded.
+  std::string device_failure() const;
+  // device_failure(), or an NCCL asynchronous error (ncclCommGetAsyncError)
+  std::string async_failure();
   struct P2PUpdate {
     const DeviceTable::Entry* tab = nullptr;  // bucket-group coordinates, sorted
     int n_entries = 0;
@@ -115,6 +132,22 @@ class Transport {
   std::mutex mu_;
   // peer-memory path
   void setup_flags();  // one flag region per communicator, shared
+  void ensure_local_flags(int comm);  // local peer mode: R regions per communicator
+  void setup_abort();
+  void serialize_launch(int comm, int rank, cudaStream_t s, bool after);
+  void wait_colocated(int comm, int rank);
+  bool local_peer_ = false;
+  std::vector<int> local_share_next_;  // local peer mode: next mailbox slot per rank
+  int flags_device_ = -1;
+  struct LaunchOrder {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev = nullptr;
+    int dev = -1;
+  };
+  std::vector<LaunchOrder> launch_order_;  // comm * kLedgerMaxRanks + rank
+  uint32_t* abort_host_ = nullptr;         // [0] abort code, [1..3] where (host-mapped)
+  uint32_t* abort_dev_ = nullptr;
+  int watch_id_ = -1;
   bool p2p_ok_ = false;
   bool nvls_ok_ = false;
   std::string name_;

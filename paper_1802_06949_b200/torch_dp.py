@@ -10,8 +10,13 @@ the producer is PyTorch autograd on its own CUDA stream:
   reference's key = layer index); the gradients live in one flat arena with
   256-B aligned slots so their device pointers never change -- or, with
   ``bucket_views=True``, directly in the KvStore's comm buckets
-  (gradient-as-bucket-view: push copies nothing; after step() the gradient
-  buffers hold aggregation results, not this rank's gradient);
+  (gradient-as-bucket-view: push copies nothing).  After step() the view
+  buffers are NOT this rank's gradient and, at world > 1, not the full sum
+  either: the fused peer kernel keeps only this rank's shard of the sum in
+  the bucket (shard_only; the rest still holds this rank's own gradient), and
+  with ``zero=True`` no sum at all (the reduction stays in registers).  Code
+  that reads p.grad after step() (clipping, logging) must read it before
+  step() or run with ``p2p=0``;
 * a post-accumulate-grad hook counts ready gradients per fusion bucket; when a
   bucket is complete it records a CUDA event on the autograd stream,
   ``Engine.import_event`` turns it into the latest write of the gradients

@@ -29,6 +29,9 @@ def _load_oracle() -> C.CDLL:
     for n in ("or_sgd_update_f64", "or_sgd_update_f32"):
         getattr(lib, n).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                     C.c_double, C.c_double]
+    lib.or_synth_expect.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_int]
     return lib
 
 
@@ -109,3 +112,30 @@ def sgd_update(w: np.ndarray, g: np.ndarray, lr: float, rescale: float, momentum
     fn = O.or_sgd_update_f64 if kind == "f64" else O.or_sgd_update_f32
     fn(_p(w), _p(g), _p(m) if m is not None else None, w.size, lr, rescale, momentum)
     return w, m
+
+
+DT = {"f64": 0, "f32": 1, "bf16": 2}
+
+
+def synth_expect(sizes, ranks: int, steps: int, *, wdt: str = "f32", gdt: str = "f32", cdt: str | None = None,
+                 lr: float = 0.1, rescale: float = 1.0 / 64, momentum: float = 0.0, seed_base: int = 1000,
+                 ref64: bool = True, threads: int = 0, keys=None):
+    """Expected weights of the synthetic model (csrc/trainer.cpp SynthModel)
+    after `steps` BACKWARD|COMM steps with the fused pull_update, every rank
+    (oracle.c or_synth_expect).  keys: indices to check (default all).
+    Returns (w in wdt, fp64 restatement or None, per-element tolerance scale
+    or None), the selected keys concatenated."""
+    import os
+    sizes = np.ascontiguousarray(sizes, dtype=np.int64)
+    ids = None if keys is None else np.ascontiguousarray(keys, dtype=np.int32)
+    total = int(sizes.sum() if ids is None else sizes[ids].sum())
+    w = np.empty(total, dtype=np.float64 if wdt == "f64" else np.float32)
+    r64 = np.empty(total, dtype=np.float64) if ref64 else None
+    sc = np.empty(total, dtype=np.float64) if ref64 else None
+    rc = O.or_synth_expect(DT[wdt], DT[gdt], DT[cdt or gdt], _p(sizes), len(sizes),
+                           _p(ids) if ids is not None else None, 0 if ids is None else len(ids), ranks, steps,
+                           seed_base, lr, rescale, momentum, _p(w), _p(r64) if ref64 else None,
+                           _p(sc) if ref64 else None, threads or (os.cpu_count() or 1))
+    if rc != 0:
+        raise RuntimeError("or_synth_expect failed")
+    return w, r64, sc

@@ -12,7 +12,7 @@ Outputs (committed, small):
   issue_kv.json         per-rank per-comm collective sequences of the trainer loop
                         shape (trainer.cpp:112-141) over K=8 synthetic keys, 2 iterations
   train_steps.npz       final fp64 weights of every rank after 3 push/pull/sgd
-                        iterations through the reference KvStore, per mode and R
+                        iterations through the reference KvStore, per mode and R in {2, 4, 8}
 """
 from __future__ import annotations
 
@@ -100,7 +100,7 @@ def main():
     arrays = {}
     sizes = np.array(TRAIN_SIZES, dtype=np.int64)
     K = len(TRAIN_SIZES)
-    for nranks in (2, 4):
+    for nranks in (2, 4, 8):
         rescale = 1.0 / (64 * nranks)
         grads = [O.random_uniform(int(sizes[k]), 1000 + r * K + k) for r in range(nranks) for k in range(K)]
         w0 = [O.random_uniform(int(sizes[k]), O.mix_seed(7, k)) for k in range(K)]

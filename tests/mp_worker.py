@@ -4,6 +4,10 @@ transport; launched by tests/test_nccl_multigpu.py through torchrun.
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P tests/mp_worker.py <case> <outdir>
 
+run_colocated() runs the same cases as rank THREADS on one GPU over a local
+peer transport (tests/test_peer_local_gpu.py): the fused peer-memory kernels
+then run on plain device pointers instead of CUDA-IPC-mapped peers.
+
 Writes <outdir>/<case>_r<rank>.npz / .json; the test compares them with the
 oracle and the golden fixtures.  torch.distributed (gloo) is plumbing only:
 it passes the ledger name and joins the ranks at the end.
@@ -32,18 +36,11 @@ def t64(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
 
 
-def main():
-    case, outdir = sys.argv[1], Path(sys.argv[2])
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    dist.init_process_group("gloo")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    name = [f"csb_test_{os.getpid()}_{time.time_ns() % 10**9}"]
-    dist.broadcast_object_list(name, src=0)
-    sink = TraceSink()
-    watchdog = 3000 if case in ("mismatch", "deadlock") else 60000
-    tr = Transport.nccl(name[0], world, rank, local, watchdog, sink)
+def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False):
+    """One rank of `case` on transport `tr` (NCCL across processes, or a local
+    peer transport shared by rank threads on one GPU when colocated).  Writes
+    the rank's .npz; returns the rank's JSON record."""
+    local = dev.index
     out = {}
 
     if case == "allreduce":
@@ -123,7 +120,7 @@ def main():
         g = torch.from_numpy(O.random_uniform(n, 1000 + rank).astype(np.float32)).to(dev)
         w0 = torch.from_numpy(O.random_uniform(n, O.mix_seed(7, 0)).astype(np.float32)).to(dev)
         buf = torch.empty(n, dtype=torch.float32, device=dev)
-        peers = tr.share_buffer(buf.data_ptr())
+        peers = tr.share_buffer(buf.data_ptr(), rank)
         res = {}
         buf.copy_(g)
         torch.cuda.synchronize(dev)
@@ -260,12 +257,58 @@ def main():
 
     if case.split("_")[0] in ("funnel", "depcha", "concom"):
         out["trace"] = [f"{e['kind']}:{e['comm']}:{e['seq']}:{e.get('key', -1)}"
-                        for e in sink.snapshot() if e["event"] == "coll_enqueued"]
+                        for e in sink.snapshot()
+                        if e["event"] == "coll_enqueued" and (not colocated or e.get("rank") == rank)]
     (outdir / f"{case}_r{rank}.json").write_text(json.dumps(out))
+    return out
+
+
+def main():
+    case, outdir = sys.argv[1], Path(sys.argv[2])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    name = [f"csb_test_{os.getpid()}_{time.time_ns() % 10**9}"]
+    dist.broadcast_object_list(name, src=0)
+    sink = TraceSink()
+    watchdog = 3000 if case in ("mismatch", "deadlock") else 60000
+    tr = Transport.nccl(name[0], world, rank, local, watchdog, sink)
+    run_rank(case, rank, world, tr, dev, outdir, sink)
     dist.barrier()
     tr.close()
     dist.destroy_process_group()
 
 
-if __name__ == "__main__":
-    main()
+def run_colocated(case, world, outdir, watchdog_ms=60000):
+    """The same case with `world` rank THREADS on cuda:0 over a local peer
+    transport: every cross-GPU kernel (fused allreduce+update, ZeRO-1, the
+    pair barriers and epochs) runs on one device, grids capped to co-reside.
+    Returns the per-rank JSON records."""
+    import threading
+    sink = TraceSink()
+    tr = Transport.local(world, watchdog_ms, sink, peer=True)
+    assert tr.p2p_capable()
+    outs, errs = [None] * world, []
+    dev = torch.device("cuda", 0)
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            # every rank thread on its own framework stream: a rank's torch work
+            # must never queue behind another rank's wait on a peer kernel
+            with torch.cuda.stream(torch.cuda.Stream(dev)):
+                outs[r] = run_rank(case, r, world, tr, dev, outdir, sink, colocated=True)
+        except BaseException as e:  # re-raised on the caller's thread
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    tr.close()
+    if errs:
+        raise errs[0]
+    return outs

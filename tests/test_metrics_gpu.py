@@ -142,3 +142,29 @@ def test_runs_are_deterministic(gpu):
     a, b = run_synthetic(**kw), run_synthetic(**kw)
     assert a.ok() and b.ok()
     assert a.b200["weight_checksums"] == b.b200["weight_checksums"]
+
+
+def test_depcha_beats_funnel_acceptance_7(gpu):
+    """acceptance.cpp:277-304 (criterion 7, the paper's central claim,
+    PAPER.md:469) over the GPU path: 2 rank threads, 5 ms injected latency per
+    collective, the 8-key diamond model, 5 runs each -- DepCha's mean epoch
+    time is strictly below Funnel's.  Funnel blocks its one communication
+    thread on every collective (kvstore.cpp:112-116), so nothing of the next
+    step is issued before the last collective is done; DepCha only chains the
+    collectives by dependency, so the next step's backward runs under them.
+    The synthetic backward (10 ms, reverse key order) stands in for the
+    reference's CPU forward/backward of the diamond model."""
+    from paper_1802_06949_b200.cli import model_sizes
+    sizes = model_sizes("diamond")
+
+    def mean_epoch(mode):
+        total = 0.0
+        for i in range(5):
+            m = run_synthetic(mode=mode, workers=2, engine_threads=4, epochs=1, steps_per_epoch=4, sizes=sizes,
+                              backward_ms=10.0, seed=100 + i, inject_latency_us=5000, global_batch=4096)
+            assert m.ok(), (m.error, m.b200)
+            total += sum(m.epoch_times_s) / len(m.epoch_times_s)  # Metrics::mean_epoch_time
+        return total / 5
+
+    funnel, depcha = mean_epoch("funnel"), mean_epoch("depcha")
+    assert depcha < funnel, f"mean epoch funnel {funnel:.4f}s vs depcha {depcha:.4f}s"

@@ -135,3 +135,43 @@ def test_bucket_map_spec():
     assert groups[1] == [3] and groups[2] == [4]
     b2, off2, groups2 = bucket_map(sizes, 4, 4096, issue_order=1)
     assert groups2[0] == [4] and groups2[1] == [3] and groups2[2] == [2, 1, 0]
+
+
+def test_synth_expect_pinned_to_reference_golden_weights():
+    """or_synth_expect (the bench / large-config parity oracle) in fp64 with
+    momentum 0 IS the reference trainer's 3-step result: equal, bit for bit,
+    to the weights the unmodified reference KvStore produced
+    (tests/golden/train_steps.npz, seeds of test_kvstore.cpp:304) at R = 2, 4, 8."""
+    gold = np.load(GOLD / "train_steps.npz")
+    sizes = [int(x) for x in gold["sizes"]]
+    for R in (2, 4, 8):
+        w, r64, _ = O.synth_expect(sizes, R, 3, wdt="f64", gdt="f64", lr=float(gold["lr"]), rescale=1.0 / (64 * R))
+        off = 0
+        for k, n in enumerate(sizes):
+            np.testing.assert_array_equal(w[off:off + n], gold[f"depcha_R{R}_r0_k{k}"])
+            np.testing.assert_array_equal(r64[off:off + n], gold[f"depcha_R{R}_r0_k{k}"])
+            off += n
+
+
+def test_synth_expect_matches_elementwise_oracle_f32_bf16():
+    """The fused fp32 / bf16 expectation equals the element-wise restatement
+    (rank_order_sum + sgd_update with momentum), and stays within the
+    north-star tolerance of its fp64 restatement (1e-6 fp32, 1e-2 bf16)."""
+    sizes, R, steps, mu = [3, 64, 1000], 4, 3, 0.9
+    K = len(sizes)
+    for gdt, tol in (("f32", 1e-6), ("bf16", 1e-2)):
+        w, r64, sc = O.synth_expect(sizes, R, steps, wdt="f32", gdt=gdt, momentum=mu, rescale=1.0 / 256)
+        off = 0
+        for k, n in enumerate(sizes):
+            gs = [O.random_uniform(n, 1000 + r * K + k).astype(np.float32) for r in range(R)]
+            if gdt == "bf16":
+                g = O.bf16_bits_to_f32(O.rank_order_sum([O.f32_to_bf16_bits(x) for x in gs], "bf16"))
+            else:
+                g = O.rank_order_sum(gs, "f32")
+            wk = O.random_uniform(n, O.mix_seed(7, k)).astype(np.float32)
+            m = np.zeros(n, np.float32)
+            for _ in range(steps):
+                wk, m = O.sgd_update(wk, g, 0.1, 1.0 / 256, mu, m, kind="f32")
+            np.testing.assert_array_equal(w[off:off + n], wk)
+            off += n
+        assert np.max(np.abs(w - r64) / sc) <= tol
