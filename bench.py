@@ -534,7 +534,7 @@ def main():
         n_prof = max(3, min(args.steps, 10))
         model.run(n_prof, COMM)
         api.profile_enable(False)
-        kstats = {k: api.profile_collect(k) for k in ("pack", "sum", "sgd")}
+        kstats = {k: api.profile_collect(k) for k in ("pack", "sum", "sgd", "pack_sgd")}
         dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
         ks = kstats[dom]
         pk = peaks()

@@ -325,7 +325,10 @@ int cs_synth_info(cs_synth_t s, uint64_t* grad_bytes, uint64_t* h2d_bytes_per_st
 int cs_synth_last_host_ms(cs_synth_t s, double* out);
 
 /* ------------------------------------------------ launch accounting */
-enum { CS_KERNEL_PACK = 0, CS_KERNEL_SUM = 1, CS_KERNEL_SGD = 2, CS_KERNEL_SYNTH = 3, CS_KERNEL_CHECKSUM = 4 };
+enum {
+  CS_KERNEL_PACK = 0, CS_KERNEL_SUM = 1, CS_KERNEL_SGD = 2, CS_KERNEL_SYNTH = 3, CS_KERNEL_CHECKSUM = 4,
+  CS_KERNEL_PACK_SGD = 5 /* (a)+(c) fused: one rank, the collective between them is the identity */
+};
 int cs_launch_count(uint64_t* out); /* kernels of this library launched so far */
 int cs_profile_enable(int on);      /* per-launch CUDA-event timing on the launch stream */
 int cs_profile_collect(int kind, uint64_t* launches, double* total_ms, double* bytes);

@@ -156,7 +156,7 @@ class SynthConfigC(C.Structure):
 
 
 CS_STEP_BACKWARD, CS_STEP_COMM, CS_STEP_LOCAL_UPDATE, CS_STEP_CHECKSUM = 1, 2, 4, 8
-KERNEL_KINDS = {"pack": 0, "sum": 1, "sgd": 2, "synth": 3, "checksum": 4}
+KERNEL_KINDS = {"pack": 0, "sum": 1, "sgd": 2, "synth": 3, "checksum": 4, "pack_sgd": 5}
 _RESTYPE = {"cs_last_error": C.c_char_p, "cs_status_name": C.c_char_p}
 
 

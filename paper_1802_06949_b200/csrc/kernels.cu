@@ -531,6 +531,97 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// (a)+(c) fused for one rank (the allreduce between them is the identity):
+// stage the gradient into its comm-bucket slot and update the weights from
+// the staged value in the same pass -- kernel (a)'s cast (comm_rounded) and
+// kernel (c)'s arithmetic on the same registers, so the result is bit for
+// bit the unfused pack -> identity -> update chain.  Entry: a = g, b = mom,
+// c = w, d = bucket slot (d == a: an in-place bucket view, no store).
+template <int CDT, typename Acc>
+__device__ __forceinline__ Acc comm_cast(Acc x) {
+  if constexpr (CDT == CS_BF16) return static_cast<Acc>(__bfloat162float(__float2bfloat16_rn(static_cast<float>(x))));
+  else if constexpr (CDT == CS_F32) return static_cast<Acc>(static_cast<float>(x));
+  else return x;
+}
+
+template <int GDT, int CDT, int WDT, bool MOM>
+__device__ __forceinline__ void pack_sgd_segment(const void* g, void* bucket, void* w, void* mom, uint64_t n,
+                                                 bool vec, uint64_t lo, uint64_t hi, double step_d, double mu_d) {
+  using Acc = typename AccOf<WDT, WDT>::T;
+  constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
+  constexpr int U = 2;
+  const Acc step = static_cast<Acc>(step_d);
+  const Acc mu = static_cast<Acc>(mu_d);
+  const bool stage = bucket != g;
+  uint64_t q = lo + threadIdx.x;
+  if (vec) {
+    const uint64_t hi_full = min(hi, n / kVec);
+    for (; q + (U - 1) * kThreads < hi_full; q += U * kThreads) {
+      Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = (q + u * kThreads) * kVec;
+        load8<GDT, Acc>(g, i, gv[u]);
+        load8_rw<WDT, Acc>(w, i, wv[u]);
+        if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = (q + u * kThreads) * kVec;
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) gv[u][j] = comm_cast<CDT>(gv[u][j]);
+        if (stage) store8<CDT, Acc>(bucket, i, gv[u]);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[u][j], gv[u][j], mv[u][j], step, mu);
+        store8<WDT, Acc>(w, i, wv[u]);
+        if constexpr (MOM) store8<MDT, Acc>(mom, i, mv[u]);
+      }
+    }
+    for (; q < hi_full; q += kThreads) {
+      const uint64_t i = q * kVec;
+      Acc gv[kVec], wv[kVec], mv[kVec];
+      load8<GDT, Acc>(g, i, gv);
+      load8_rw<WDT, Acc>(w, i, wv);
+      if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) gv[j] = comm_cast<CDT>(gv[j]);
+      if (stage) store8<CDT, Acc>(bucket, i, gv);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[j], gv[j], mv[j], step, mu);
+      store8<WDT, Acc>(w, i, wv);
+      if constexpr (MOM) store8<MDT, Acc>(mom, i, mv);
+    }
+  }
+  for (; q < hi; q += kThreads) {
+    const uint64_t end = min(n, (q + 1) * kVec);
+    for (uint64_t j = q * kVec; j < end; ++j) {
+      const Acc gg = comm_cast<CDT>(load1<GDT, Acc>(g, j));
+      if (stage) store1<CDT, Acc>(bucket, j, gg);
+      Acc ww = load1<WDT, Acc>(w, j), mm = Acc(0);
+      if constexpr (MOM) mm = load1<MDT, Acc>(mom, j);
+      sgd_elem<MOM>(ww, gg, mm, step, mu);
+      if constexpr (MOM) store1<MDT, Acc>(mom, j, mm);
+      store1<WDT, Acc>(w, j, ww);
+    }
+  }
+}
+
+template <int GDT, int CDT, int WDT, bool MOM>
+__global__ void __launch_bounds__(kThreads)
+    pack_sgd_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
+                        const uint8_t* __restrict__ vec, uint64_t total, double step, double mu) {
+  uint64_t g0, g1;
+  cta_range(total, g0, g1);
+  if (g0 >= g1) return;
+  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
+    const DevEntry en = tab[e];
+    const uint64_t hi = min(g1, en.gend);
+    pack_sgd_segment<GDT, CDT, WDT, MOM>(en.a, en.d, en.c, const_cast<void*>(en.b), en.n, vec[e],
+                                         g0 - en.gstart, hi - en.gstart, step, mu);
+    g0 = hi;
+  }
+}
+
 // ------------------------- fused NVLink allreduce (+ SGD) over peer memory
 //
 // One kernel per bucket per rank, all ranks launched with the same grid G
@@ -579,6 +670,7 @@ struct P2PParams {
   double step, mu;
   int nranks, rank, n_entries, shard_only;
   int sys_fence;  // explicit fence.sc.sys before the release store of a pair barrier (CSB_P2P_FENCE)
+  int pack;       // stage the gradients (entry d) into this rank's bucket (entry a) before barrier 0
   uint32_t epoch;
 };
 
@@ -744,6 +836,44 @@ __device__ __forceinline__ void nvls_reduce_chunk(const P2PParams& p, uint64_t a
   }
 }
 
+// Kernel (a) folded into the peer kernels' phase 0.  CTA c stages column c
+// of this rank's bucket -- chunk c of every shard, exactly the groups the
+// peers' CTA c read from this bucket after the pair barrier -- from the
+// gradients (entry d) into the bucket slots (entry a), on all 512 threads.
+// The pair barrier that follows is the one the separate pack kernel's
+// completion used to satisfy, so no launch, stream hop or extra barrier is
+// added, and CTAs that finish staging early start reducing while others
+// still stage.
+template <int CDT>
+__device__ __forceinline__ void p2p_pack_range(const P2PParams& p, uint64_t a, uint64_t b) {
+  if (a >= b || p.n_entries == 0) return;
+  int lo = 0, hi = p.n_entries;  // first entry with gend > a
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p.tab[mid].gend <= a) lo = mid + 1;
+    else hi = mid;
+  }
+  for (int e = lo; e < p.n_entries; ++e) {
+    const DevEntry en = p.tab[e];
+    if (en.gstart >= b) break;
+    if (!en.d || en.d == en.a) continue;  // a bucket view: already in place
+    const uint64_t s0 = max(a, en.gstart), s1 = min(b, en.gend);
+    const bool vec = ((reinterpret_cast<uintptr_t>(en.a) | reinterpret_cast<uintptr_t>(en.d)) & 15u) == 0;
+    pack_segment<CDT, CDT, kP2PThreads>(en.d, const_cast<void*>(en.a), en.n, vec, s0 - en.gstart,
+                                        s1 - en.gstart);
+  }
+}
+
+template <int CDT>
+__device__ __forceinline__ void p2p_pack_column(const P2PParams& p) {
+  const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
+  for (int k = 0; k < p.nranks; ++k) {
+    const int s = (p.rank + k) % p.nranks;  // own shard first
+    const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
+    p2p_pack_range<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
+  }
+}
+
 // SGD over bucket groups [a, b) of shard `owner` through the entries
 // (bucket-group coordinates).  shard_only: the reduced gradient of another
 // owner's shard is read from that owner's bucket over NVLink.
@@ -775,6 +905,9 @@ template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
   const uint64_t T = p.groups;
   const uint64_t G = gridDim.x, c = blockIdx.x;
+  if constexpr (UPDATE && !NVLS) {
+    if (p.pack) p2p_pack_column<CDT>(p);
+  }
   if (!pair_barrier(p, 0)) return;
   {
     const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
@@ -902,6 +1035,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_c
     b = s0 + L * (c + 1) / G;
   };
   uint64_t s0, a, b;
+  if (p.pack) p2p_pack_column<CDT>(p);
   if (!pair_barrier(p, 0)) return;
   chunk(p.rank, s0, a, b);
   zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b);
@@ -1443,6 +1577,64 @@ void DeviceTable::sgd(const cs_update_entry* es, int n, int wdt, int gdt, double
                    " g=" + dtype_name(gdt));
 }
 
+bool DeviceTable::pack_sgd_supported(int gdt, int cdt, int wdt) {
+  return (gdt == CS_F32 && cdt == CS_F32 && wdt == CS_F32) || (gdt == CS_BF16 && cdt == CS_BF16 && wdt == CS_F32) ||
+         (gdt == CS_F32 && cdt == CS_BF16 && wdt == CS_F32) || (gdt == CS_BF16 && cdt == CS_F32 && wdt == CS_F32) ||
+         (gdt == CS_F64 && cdt == CS_F64 && wdt == CS_F64);
+}
+
+void DeviceTable::pack_sgd(const std::vector<PackUpdate>& es, int gdt, int cdt, int wdt, double lr, double rescale,
+                           double momentum, cudaStream_t s) {
+  if (!pack_sgd_supported(gdt, cdt, wdt)) throw UsageError("pack_sgd: unsupported dtype combination");
+  host_.clear();
+  vec_.clear();
+  groups_ = 0;
+  const bool mom = momentum != 0.0;
+  double bytes = 0;
+  for (const PackUpdate& e : es) {
+    if (e.n == 0) continue;
+    if (!e.g || !e.bucket || !e.w) throw UsageError("pack_sgd: null pointer in entry");
+    if (mom && !e.mom) throw UsageError("pack_sgd: momentum > 0 needs a momentum buffer");
+    const uint64_t g = groups_of(e.n);
+    Entry en{e.g, e.mom, e.w, e.n, groups_, groups_ + g};
+    en.d = e.bucket;
+    host_.push_back(en);
+    vec_.push_back(aligned16(e.g) && aligned16(e.bucket) && aligned16(e.w) && (!mom || aligned16(e.mom)));
+    groups_ += g;
+    bytes += static_cast<double>(e.n) *
+             (dtype_size(gdt) + (e.bucket != e.g ? dtype_size(cdt) : 0) + 2.0 * dtype_size(wdt) +
+              (mom ? 2.0 * (wdt == CS_F64 ? 8 : 4) : 0.0));
+  }
+  if (host_.empty()) return;
+  const double step = lr * rescale;  // model.cpp:21, fp64 on the host
+  LaunchScope ls(kKernPackSgd, bytes, s);
+#define CSB_PACK_SGD(G, C, W, M)                                                              \
+  if (gdt == G && cdt == C && wdt == W && mom == M) {                                         \
+    grid_ = wave_grid(pack_sgd_tab_kernel<G, C, W, M>, groups_);                              \
+    sync(nullptr, s);                                                                         \
+    const char* base = static_cast<const char*>(dev_);                                        \
+    pack_sgd_tab_kernel<G, C, W, M><<<grid_, kThreads, 0, s>>>(                               \
+        reinterpret_cast<const Entry*>(base),                                                 \
+        reinterpret_cast<const uint32_t*>(base + host_.size() * sizeof(Entry)),               \
+        reinterpret_cast<const uint8_t*>(base + host_.size() * sizeof(Entry) + first_.size() * 4), \
+        groups_, step, momentum);                                                             \
+    check_launch("pack_sgd_tab_kernel");                                                      \
+    ls.done();                                                                                \
+    return;                                                                                   \
+  }
+  CSB_PACK_SGD(CS_F32, CS_F32, CS_F32, false)
+  CSB_PACK_SGD(CS_F32, CS_F32, CS_F32, true)
+  CSB_PACK_SGD(CS_BF16, CS_BF16, CS_F32, false)
+  CSB_PACK_SGD(CS_BF16, CS_BF16, CS_F32, true)
+  CSB_PACK_SGD(CS_F32, CS_BF16, CS_F32, false)
+  CSB_PACK_SGD(CS_F32, CS_BF16, CS_F32, true)
+  CSB_PACK_SGD(CS_BF16, CS_F32, CS_F32, false)
+  CSB_PACK_SGD(CS_BF16, CS_F32, CS_F32, true)
+  CSB_PACK_SGD(CS_F64, CS_F64, CS_F64, false)
+  CSB_PACK_SGD(CS_F64, CS_F64, CS_F64, true)
+#undef CSB_PACK_SGD
+}
+
 const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cudaStream_t s) {
   host_ = es;
   vec_.assign(es.size(), 0);
@@ -1510,6 +1702,7 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   p.rank = a.rank;
   p.epoch = a.epoch;
   p.shard_only = (a.shard_only && a.update && !a.mc) ? 1 : 0;
+  p.pack = (a.pack && a.update && a.tab && a.n_entries > 0 && !a.mc) ? 1 : 0;
   const bool zero = a.zero && a.update && !a.mc;
   if (a.zero && !zero) throw UsageError("p2p_allreduce: ZeRO-1 needs the fused update over peer memory");
   for (int r = 0; zero && r < a.nranks; ++r) {

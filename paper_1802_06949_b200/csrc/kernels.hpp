@@ -34,14 +34,33 @@ class DeviceTable {
   void pack(const cs_copy_entry* es, int n, int src_dt, int dst_dt, cudaStream_t s);
   void sgd(const cs_update_entry* es, int n, int w_dt, int g_dt, double lr, double rescale,
            double momentum, cudaStream_t s);
+  // Kernel (a) fused with kernel (c) when the collective between them is the
+  // identity (one rank): every entry's gradient (g_dt) is staged into its
+  // comm-bucket slot (c_dt, the copy of kvstore.cpp:109) and, from the same
+  // registers, the weights are updated with the staged value -- one pass
+  // instead of a pack launch plus an update launch that re-reads the bucket.
+  // es[i]: g = gradient, mom, w = weights, bucket = the key's comm slot
+  // (may equal g: an in-place bucket view, nothing to stage).
+  struct PackUpdate {
+    const void* g;
+    void* bucket;
+    void* w;
+    void* mom;
+    uint64_t n;
+  };
+  static bool pack_sgd_supported(int g_dt, int c_dt, int w_dt);
+  void pack_sgd(const std::vector<PackUpdate>& es, int g_dt, int c_dt, int w_dt, double lr, double rescale,
+                double momentum, cudaStream_t s);
   uint64_t uploads() const { return uploads_; }
 
-  struct Entry {  // 48 B; a/b/c per kernel: pack a=src c=dst; sgd a=g b=mom c=w
+  struct Entry {  // 56 B; a/b/c/d per kernel: pack a=src c=dst; sgd a=g b=mom c=w;
+                  // pack_sgd a=g b=mom c=w d=comm-bucket slot
     const void* a;
     const void* b;
     void* c;
     uint64_t n;
     uint64_t gstart, gend;
+    void* d = nullptr;
   };
   // Keeps `es` resident (uploading on change) and returns the device copy.
   const Entry* resident(const std::vector<Entry>& es, cudaStream_t s);
@@ -75,6 +94,9 @@ struct P2PArgs {
   int n_entries = 0;
   bool update = false;
   bool shard_only = false;  // phase 1 stores only the own shard; the update reads the owners' buckets
+  // stage the gradients (entry d, the comm dtype) into this rank's bucket
+  // slots (entry a) inside the kernel, before barrier 0 (kernel (a) folded in)
+  bool pack = false;
   // ZeRO-1: master-weight shards of every rank and this rank's momentum shard
   // (shard-local layout, p2p_shard_elems each); weights all-gathered after the update
   bool zero = false;
@@ -102,7 +124,9 @@ void p2p_allreduce(const P2PArgs& args, cudaStream_t s);
 uint64_t p2p_timeout_ns();
 
 // Launch accounting and optional per-launch CUDA-event timing (roofline).
-enum KernelKind { kKernPack = 0, kKernSum = 1, kKernSgd = 2, kKernSynth = 3, kKernChecksum = 4, kKernKinds = 5 };
+enum KernelKind {
+  kKernPack = 0, kKernSum = 1, kKernSgd = 2, kKernSynth = 3, kKernChecksum = 4, kKernPackSgd = 5, kKernKinds = 6
+};
 struct KernelStats {
   uint64_t launches = 0;
   double total_ms = 0.0;  // summed CUDA-event durations (profiling on only)

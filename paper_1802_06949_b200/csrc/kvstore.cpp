@@ -79,6 +79,19 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   // one rank: nothing crosses NVLink, the collectives are the identity
   p2p_active_ = cfg_.p2p != 0 && transport_.p2p_capable();
   zero_active_ = p2p_active_ && cfg_.zero;
+  static const bool n1_fuse = [] {
+    const char* e = std::getenv("CSB_N1_FUSE");
+    return !(e && std::string(e) == "0");
+  }();
+  // and across GPUs: DepCha's whole-bucket fused peer kernel stages the
+  // gradients itself (CTA c packs the column its peers read after barrier 0)
+  static const bool p2p_fuse = [] {
+    const char* e = std::getenv("CSB_P2P_FUSE_PACK");
+    return !(e && std::string(e) == "0");
+  }();
+  defer_pack_ = (n1_fuse && transport_.num_ranks() == 1 &&
+                 (cfg_.mode == KvMode::DepCha || cfg_.mode == KvMode::Naive)) ||
+                (p2p_fuse && p2p_active_ && cfg_.mode == KvMode::DepCha && cfg_.p2p == 1);
   if (engine_.device() < 0) throw ConfigError("KvStore: the engine must be bound to a CUDA device");
   keys_.resize(static_cast<size_t>(cfg_.num_keys));
   init_order_tag_ = engine_.new_variable();
@@ -380,22 +393,53 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
       reads.push_back(g.tag);
       keys_[static_cast<size_t>(k)].pushed = true;
     }
-    muts.push_back(B.tag);
-    const int dst_dt = comm_dt_;
     const int key0 = keys[static_cast<size_t>(idxs[0])];
-    if (!B.pack_tab) B.pack_tab = std::make_shared<DeviceTable>();
-    DeviceTable* tab = B.pack_tab.get();  // resident table; all its launches on pack_lane_
-    engine_.push_stream(
-        [entries, src_dt, dst_dt, tab](cudaStream_t s) {
-          if (!entries.empty()) tab->pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
-        },
-        reads, muts, OpKind::Copy, key0, pack_lane_, Dispatch::Inline);
+    if (defer_pack_ && (B.deferred_dt < 0 || B.deferred_dt == src_dt)) {
+      // one rank: stage at the pull_update, fused with the update (or flushed
+      // as this very pack op by any other use of the bucket)
+      size_t j = 0;
+      for (int i : idxs) {
+        const int k = keys[static_cast<size_t>(i)];
+        const TensorSlot& g = grads[static_cast<size_t>(i)];
+        if (g.data == key_ptr(k) && g.dtype == comm_dt_) continue;  // a bucket view
+        B.deferred.push_back({k, entries[j++]});
+      }
+      B.deferred_reads.insert(B.deferred_reads.end(), reads.begin(), reads.end());
+      B.deferred_dt = src_dt;
+    } else {
+      flush_deferred(B);
+      push_pack_op(B, entries, reads, src_dt, key0);
+    }
     B.pushed += static_cast<int>(idxs.size());
 
     if (B.pushed == static_cast<int>(B.keys.size()) &&
         (cfg_.mode == KvMode::Funnel || cfg_.mode == KvMode::ConCom))
       issue_collective(b, reads);
   }
+}
+
+// kernel (a): stage the listed gradients into their bucket slots, one launch
+// (kvstore.cpp:109 `copy(g, comm_buf)`), ordered after the gradients' writes
+void KvStore::push_pack_op(Bucket& B, const std::vector<cs_copy_entry>& entries, const std::vector<Tag>& reads,
+                           int src_dt, int key0) {
+  const int dst_dt = comm_dt_;
+  if (!B.pack_tab) B.pack_tab = std::make_shared<DeviceTable>();
+  DeviceTable* tab = B.pack_tab.get();  // resident table; all its launches on pack_lane_
+  engine_.push_stream(
+      [entries, src_dt, dst_dt, tab](cudaStream_t s) {
+        if (!entries.empty()) tab->pack(entries.data(), static_cast<int>(entries.size()), src_dt, dst_dt, s);
+      },
+      reads, {B.tag}, OpKind::Copy, key0, pack_lane_, Dispatch::Inline);
+}
+
+void KvStore::flush_deferred(Bucket& B) {
+  if (B.deferred.empty() && B.deferred_reads.empty()) return;
+  std::vector<cs_copy_entry> entries;
+  for (const auto& [k, e] : B.deferred) entries.push_back(e);
+  push_pack_op(B, entries, B.deferred_reads, B.deferred_dt, B.deferred.empty() ? B.keys[0] : B.deferred[0].first);
+  B.deferred.clear();
+  B.deferred_reads.clear();
+  B.deferred_dt = -1;
 }
 
 void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
@@ -508,6 +552,15 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     Bucket& B = buckets_[static_cast<size_t>(b)];
     if (B.pushed != static_cast<int>(B.keys.size()))
       throw UsageError("KvStore: pull of a fusion bucket before all of its keys were pushed");
+    // one rank: a whole-bucket pull_update (into the comm dtype's supported
+    // weights) stages and updates in one kernel; anything else packs first
+    const bool whole_upd = sgd && !B.issued && B.pulled == 0 && idxs.size() == B.keys.size();
+    const bool deferred = !B.deferred_reads.empty();
+    const bool fuse = deferred && whole_upd && !p2p_active_ &&
+                      DeviceTable::pack_sgd_supported(B.deferred_dt < 0 ? comm_dt_ : B.deferred_dt, comm_dt_,
+                                                      outs[static_cast<size_t>(idxs[0])].dtype);
+    const bool fuse_p2p = deferred && whole_upd && p2p_active_ && (B.deferred_dt < 0 || B.deferred_dt == comm_dt_);
+    if (!fuse && !fuse_p2p) flush_deferred(B);
     std::vector<Tag> buf_tags{B.tag}, out_tags;
     for (const Tag& t : B.view_tags) buf_tags.push_back(t);
     std::vector<cs_copy_entry> copies;
@@ -570,10 +623,21 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         // the reduced gradient from the local bucket), mutating the weights
         std::vector<DeviceTable::Entry> es;
         for (size_t j = 0; j < updates.size(); ++j) {
-          const KeyState& ks = keys_[static_cast<size_t>(keys[static_cast<size_t>(idxs[j])])];
+          const int k = keys[static_cast<size_t>(idxs[j])];
+          const KeyState& ks = keys_[static_cast<size_t>(k)];
           const uint64_t g0 = ks.offset / 8;
           es.push_back(DeviceTable::Entry{updates[j].g, updates[j].mom, updates[j].w, updates[j].n, g0,
                                           g0 + (updates[j].n + 7) / 8});
+          if (fuse_p2p)  // the kernel stages this key's gradient (d) into its slot (a)
+            for (const auto& [dk, e] : B.deferred)
+              if (dk == k) es.back().d = const_cast<void*>(e.src);
+        }
+        std::vector<Tag> p2p_reads;
+        if (fuse_p2p) {
+          p2p_reads = B.deferred_reads;
+          B.deferred.clear();
+          B.deferred_reads.clear();
+          B.deferred_dt = -1;
         }
         std::sort(es.begin(), es.end(), [](const auto& x, const auto& y) { return x.gstart < y.gstart; });
         if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
@@ -581,7 +645,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         for (const Tag& t : out_tags) muts.push_back(t);
         const bool zero = zero_active_;
         engine_.push_stream(
-            [self, bi, es, ptab, out_dt, opt, whole, zero](cudaStream_t s) {
+            [self, bi, es, ptab, out_dt, opt, whole, zero, fuse_p2p](cudaStream_t s) {
               Bucket& Bk = self->buckets_[bi];
               Transport::P2PUpdate u;
               u.tab = ptab->resident(es, s);
@@ -591,6 +655,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
               u.rescale = opt.rescale;
               u.momentum = opt.momentum;
               u.shard_only = whole;
+              u.pack = fuse_p2p;
               if (zero) {
                 if (!Bk.master_ready) self->zero_fill_master(Bk, es, out_dt, s);
                 u.wm = Bk.wm_peers.data();
@@ -598,7 +663,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
               }
               self->collective_body(Bk, bi, s, &u);
             },
-            {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
+            p2p_reads, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
         for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;
         B.pulled += static_cast<int>(idxs.size());
         if (B.pulled == static_cast<int>(B.keys.size())) {
@@ -612,8 +677,37 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       engine_.push_stream([self, bi](cudaStream_t s) { self->collective_body(self->buckets_[bi], bi, s, nullptr); },
                           {}, muts, OpKind::Collective, ckey, B.lane, depcha_dispatch());
     }
-    engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
-                        update_lane_, Dispatch::Inline);
+    if (fuse) {
+      // (a)+(c) in one op after the (identity) collective: reads the pushed
+      // gradients, writes the bucket and the weights
+      std::vector<DeviceTable::PackUpdate> pu;
+      for (int i : idxs) {
+        const int k = keys[static_cast<size_t>(i)];
+        const TensorSlot& o = outs[static_cast<size_t>(i)];
+        const void* g = key_ptr(k);  // a bucket view: already in place
+        for (const auto& [dk, e] : B.deferred)
+          if (dk == k) g = e.src;
+        pu.push_back(DeviceTable::PackUpdate{g, key_ptr(k), o.data, keys_[static_cast<size_t>(k)].mom, o.numel});
+      }
+      std::vector<Tag> reads = B.deferred_reads;
+      for (const Tag& t : B.view_tags) reads.push_back(t);
+      std::vector<Tag> fmuts{B.tag};
+      for (const Tag& t : out_tags) fmuts.push_back(t);
+      if (!B.fused_tab) B.fused_tab = std::make_shared<DeviceTable>();
+      DeviceTable* ftab = B.fused_tab.get();  // resident table, update lane only
+      const int gdt = B.deferred_dt < 0 ? comm_dt_ : B.deferred_dt;
+      engine_.push_stream(
+          [pu, gdt, cdt, out_dt, opt, ftab](cudaStream_t s) {
+            ftab->pack_sgd(pu, gdt, cdt, out_dt, opt.lr, opt.rescale, opt.momentum, s);
+          },
+          reads, fmuts, OpKind::Compute, key0, update_lane_, Dispatch::Inline);
+      B.deferred.clear();
+      B.deferred_reads.clear();
+      B.deferred_dt = -1;
+    } else {
+      engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
+                          update_lane_, Dispatch::Inline);
+    }
     for (int i : idxs) keys_[static_cast<size_t>(keys[static_cast<size_t>(i)])].pushed = false;
     B.pulled += static_cast<int>(idxs.size());
     if (B.pulled == static_cast<int>(B.keys.size())) {
@@ -637,6 +731,7 @@ void KvStore::comm_buf(int key, void* host_out) {
   check_key(key, true);
   const KeyState& ks = keys_[static_cast<size_t>(key)];
   if (ks.bucket < 0) throw UsageError("KvStore: comm buffer not allocated yet");
+  flush_deferred(buckets_[static_cast<size_t>(ks.bucket)]);
   engine_.wait_for(buckets_[static_cast<size_t>(ks.bucket)].tag);
   engine_.bind_device();
   CSB_CUDA(cudaMemcpy(host_out, key_ptr(key), ks.numel * dtype_size(comm_dt_), cudaMemcpyDeviceToHost));

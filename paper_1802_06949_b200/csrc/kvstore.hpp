@@ -147,6 +147,14 @@ class KvStore {
     std::vector<const void*> wm_peers;
     void* mom_b = nullptr;
     bool master_ready = false;
+    // One rank (the allreduce is the identity): DepCha's staging copy is
+    // deferred from push to the pull_update and fused with the update in one
+    // kernel (DeviceTable::pack_sgd); any other use of the bucket flushes it
+    // as the ordinary pack op first.
+    std::vector<std::pair<int, cs_copy_entry>> deferred;  // (key, staging copy)
+    std::vector<Tag> deferred_reads;                      // the pushed gradients' tags
+    int deferred_dt = -1;
+    std::shared_ptr<DeviceTable> fused_tab;
   };
 
   void check_key(int key, bool must_be_initialized) const;
@@ -165,6 +173,9 @@ class KvStore {
   Dispatch depcha_dispatch() const;
   void collective_body(const Bucket& B, int bucket_id, cudaStream_t s, const Transport::P2PUpdate* upd);
   void zero_fill_master(Bucket& B, const std::vector<DeviceTable::Entry>& es, int wdt, cudaStream_t s);
+  void push_pack_op(Bucket& B, const std::vector<cs_copy_entry>& entries, const std::vector<Tag>& reads, int src_dt,
+                    int key0);
+  void flush_deferred(Bucket& B);
 
   Engine& engine_;
   Transport& transport_;
@@ -189,6 +200,7 @@ class KvStore {
   void* arena_ = nullptr;
   uint64_t arena_bytes_ = 0;
   bool zero_active_ = false;  // ZeRO-1 (cfg_.zero over an active peer-memory path)
+  bool defer_pack_ = false;   // one rank, DepCha / naive: pack fused into the pull_update (CSB_N1_FUSE=0: off)
   std::vector<std::vector<void*>> shared_;  // share_buffer results, unmapped at destruction
   int zero_wdt_ = -1;
   std::vector<uint32_t> seen_;  // duplicate-key detection in one call

@@ -371,6 +371,7 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     a.rescale = upd->rescale;
     a.momentum = upd->momentum;
     a.shard_only = upd->shard_only && !mc;
+    a.pack = upd->pack && !mc;
     if (upd->wm) {
       a.zero = true;
       for (int r = 0; r < num_ranks(); ++r) a.wm[r] = const_cast<void*>(upd->wm[r]);

@@ -100,6 +100,7 @@ class Transport {
     int wdt = CS_F32;
     double lr = 0, rescale = 0, momentum = 0;
     bool shard_only = false;  // the bucket keeps only this rank's shard (update reads owners)
+    bool pack = false;        // entries' d = gradients: the kernel stages them first (kernel (a) folded in)
     const void* const* wm = nullptr;  // ZeRO-1: every rank's master shard; null = replicated update
     void* mom_b = nullptr;            // ZeRO-1: this rank's momentum shard
   };

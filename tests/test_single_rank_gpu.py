@@ -1,0 +1,84 @@
+"""One rank (the allreduce is the identity, collective.cpp:228-243 with R = 1):
+DepCha's staging copy (kernel (a), kvstore.cpp:109) is deferred from push to
+the whole-bucket pull_update and fused with the update (kernel (c),
+model.cpp:17-27) in one kernel.  These tests pin the fused kernel bit for
+bit to the oracle (or_synth_expect, itself pinned to the reference's golden
+weights), and check every other use of the bucket still sees the staged
+gradient (the deferred copy is flushed as the ordinary pack op)."""
+import numpy as np
+import pytest
+import torch
+
+import _oracle as O
+
+pytestmark = pytest.mark.gpu
+SIZES = [1, 7, 64, 300, 4097, 70000, 1 << 18]
+
+
+@pytest.mark.parametrize("wdt,gdt,cdt,mu", [("f32", "f32", "f32", 0.9), ("f32", "f32", "f32", 0.0),
+                                            ("f32", "bf16", "bf16", 0.9), ("f32", "f32", "bf16", 0.9),
+                                            ("f64", "f64", "f64", 0.0), ("f64", "f64", "f64", 0.9)])
+@pytest.mark.parametrize("bucket_bytes", [1 << 20, 0])
+def test_fused_pack_update_matches_oracle(gpu, wdt, gdt, cdt, mu, bucket_bytes):
+    from paper_1802_06949_b200 import Engine, Transport, api
+    D = {"f64": api.F64, "f32": api.F32, "bf16": api.BF16}
+    tr = Transport.local(1, 10000)
+    eng = Engine(2, 0, None, 0)
+    m = api.SynthModel(eng, tr, 0, 1, SIZES, mode="depcha", w_dtype=D[wdt], g_dtype=D[gdt], comm_dtype=D[cdt],
+                       bucket_bytes=bucket_bytes, issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=mu)
+    m.init()
+    nb = m.info()["num_buckets"]
+    api.profile_reset()
+    api.profile_enable(True)
+    m.run(3, m.BACKWARD | m.COMM)
+    api.profile_enable(False)
+    fused = api.profile_collect("pack_sgd")["launches"]
+    packs = api.profile_collect("pack")["launches"]
+    w = m.read_weights()
+    m.close()
+    eng.close()
+    tr.close()
+    exp, r64, sc = O.synth_expect(SIZES, 1, 3, wdt=wdt, gdt=gdt, cdt=cdt, lr=0.1, rescale=1.0 / 64, momentum=mu)
+    np.testing.assert_array_equal(w, exp)
+    assert np.max(np.abs(w.astype(np.float64) - r64) / sc) <= (1e-2 if "bf16" in (gdt, cdt) else 1e-6)
+    assert fused == 3 * nb and packs == 0, (fused, packs)
+
+
+def test_other_uses_of_the_bucket_see_the_staged_gradient(gpu):
+    """comm_buf after push, a plain pull, and pull_updates that split a
+    bucket all flush the deferred copy as the pack op: kvstore.cpp:109's
+    copy is never skipped, only fused when nothing else reads the bucket."""
+    from paper_1802_06949_b200 import Engine, KvConfig, KvStore, Slot, Transport, api
+    tr = Transport.local(1, 10000)
+    eng = Engine(2, 0, None, 0)
+    K = len(SIZES)
+    f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    store = KvStore(eng, tr, 0, KvConfig("depcha", 1, K, bucket_bytes=1 << 20, issue_order=1))
+    ws = [Slot(f32(O.random_uniform(n, O.mix_seed(7, k))), eng.new_variable()) for k, n in enumerate(SIZES)]
+    gs = [Slot(f32(O.random_uniform(n, 1000 + k)), eng.new_variable()) for k, n in enumerate(SIZES)]
+    for k in range(K):
+        store.init(k, ws[k])
+    eng.wait_all()
+    # 1) comm_buf right after push holds the gradient
+    store.push(list(range(K)), gs)
+    np.testing.assert_array_equal(store.comm_buf(3), gs[3].value.cpu().numpy())
+    store.pull_update(list(range(K)), ws, 0.1, 1.0 / 64, 0.0)
+    # 2) one pull_update per key (buckets not whole): pack op, then updates
+    store.push(list(range(K)), gs)
+    for k in range(K):
+        store.pull_update(k, ws[k], 0.1, 1.0 / 64, 0.0)
+    # 3) a plain pull returns the (identity-reduced) gradient
+    outs = [Slot(torch.zeros(n, dtype=torch.float32, device="cuda"), eng.new_variable()) for n in SIZES]
+    store.push(list(range(K)), gs)
+    store.pull(list(range(K)), outs)
+    eng.wait_all()
+    for k, n in enumerate(SIZES):
+        np.testing.assert_array_equal(outs[k].value.cpu().numpy(), gs[k].value.cpu().numpy())
+        w = O.random_uniform(n, O.mix_seed(7, k)).astype(np.float32)
+        g = O.random_uniform(n, 1000 + k).astype(np.float32)
+        for _ in range(2):
+            w, _ = O.sgd_update(w, g, 0.1, 1.0 / 64, kind="f32")
+        np.testing.assert_array_equal(ws[k].value.cpu().numpy(), w)
+    store.close()
+    eng.close()
+    tr.close()
