@@ -254,15 +254,24 @@ __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
-// ------------------------------------------------------- table lookup
+// ------------------------------------------------------- work split
 
 // Work is counted in GROUPS of kVec = 8 consecutive elements (one or more
 // 16-byte vectors).  A launch covers the concatenation of its table's
-// entries, T groups in total, split EVENLY over a single wave of CTAs
-// (grid = SMs x resident CTAs): CTA c owns groups [T*c/G, T*(c+1)/G), which
-// may span several entries.  Every CTA therefore moves the same number of
-// bytes and finishes together -- no wave-quantization tail, the dominant
-// loss of a chunk-per-CTA grid on buckets of a few thousand chunks.
+// entries, T groups in total, dealt out in CHUNKS of kThreads x U groups:
+// chunk j goes to CTA j mod G (a grid-stride over chunks; G = SMs x resident
+// CTAs, one wave).  At any moment the G CTAs therefore stream G neighbouring
+// chunks, so the whole GPU walks every array front to back and the DRAM rows
+// it opens are shared by many CTAs.  Round 1 gave each CTA one contiguous
+// range instead (T*c/G .. T*(c+1)/G); tools/streambench.cu measured that
+// 10-25 % slower on B200 (the fused 24 B/element pattern: 4.7-5.5 TB/s
+// contiguous vs 6.1-6.3 TB/s interleaved), the G concurrent streams per
+// array each opening their own DRAM rows.
+//
+// A thread resolves its group's table entry per chunk: the host precomputes
+// first[j], the entry holding chunk j's first group, so a chunk inside one
+// key (the common case) needs no search and a chunk spanning small keys a
+// binary search over just those keys.
 
 __device__ __forceinline__ int find_entry(const uint64_t* group_start, int n_entries, uint64_t g) {
   // largest e with group_start[e] <= g (group_start[0] = 0; entries non-empty)
@@ -273,6 +282,67 @@ __device__ __forceinline__ int find_entry(const uint64_t* group_start, int n_ent
     else hi = mid - 1;
   }
   return lo;
+}
+
+// One table entry as a walker sees it: a/b/c/d per kernel (see DeviceTable::Entry).
+struct Ent {
+  const void* a;
+  const void* b;
+  void* c;
+  void* d;
+  uint64_t n, gstart;
+  bool vec;
+};
+
+// Entries of a device-resident table (DeviceTable): first[j] = entry of
+// chunk j's first group, first[nchunks] = the last entry.
+struct TabView {
+  const DeviceTable::Entry* __restrict__ tab;
+  const uint32_t* __restrict__ first;
+  const uint8_t* __restrict__ vecf;
+  __device__ __forceinline__ Ent resolve(uint64_t j, uint64_t q) const {
+    int lo = static_cast<int>(first[j]), hi = static_cast<int>(first[j + 1]);
+    while (lo < hi) {  // largest e in [lo, hi] with gstart <= q
+      const int mid = (lo + hi + 1) >> 1;
+      if (tab[mid].gstart <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const DeviceTable::Entry& en = tab[lo];
+    return Ent{en.a, en.b, en.c, en.d, en.n, en.gstart, vecf[lo] != 0};
+  }
+};
+
+// 16-byte vector IO for data touched once per launch: streaming
+// (evict-first) loads and stores, explicitly global (LDG/STG, no generic
+// address resolution).
+template <int DT, typename Acc>
+__device__ __forceinline__ void load8s(const void* base, uint64_t i, Acc (&v)[kVec]) {
+  load8<DT, Acc>(base, i, v);  // __ldcs: ld.global.cs
+}
+
+template <int DT, typename Acc>
+__device__ __forceinline__ void store8s(void* base, uint64_t i, const Acc (&v)[kVec]) {
+  if constexpr (DT == CS_F64) {
+    double2* p = reinterpret_cast<double2*>(static_cast<double*>(base) + i);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      __stcs(p + q, make_double2(from_acc<double>(v[2 * q]), from_acc<double>(v[2 * q + 1])));
+  } else if constexpr (DT == CS_F32) {
+    float4* p = reinterpret_cast<float4*>(static_cast<float*>(base) + i);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      __stcs(p + q, make_float4(from_acc<float>(v[4 * q]), from_acc<float>(v[4 * q + 1]),
+                                from_acc<float>(v[4 * q + 2]), from_acc<float>(v[4 * q + 3])));
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 h = __halves2bfloat162(from_acc<__nv_bfloat16>(v[2 * q]),
+                                            from_acc<__nv_bfloat16>(v[2 * q + 1]));
+      w[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    __stcs(reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + i), make_uint4(w[0], w[1], w[2], w[3]));
+  }
 }
 
 __device__ __forceinline__ void cta_range(uint64_t T, uint64_t& g0, uint64_t& g1) {
@@ -322,19 +392,59 @@ __device__ __forceinline__ void pack_segment(const void* src, void* dst, uint64_
   }
 }
 
+// Walkers: U groups per thread per chunk, every load of the chunk issued
+// before its first store.  `full` groups (8 elements present, 16-B aligned
+// pointers) move as 16-B vectors, the rest element by element.
+template <int SDT, int DDT, int U, typename View>
+__device__ __forceinline__ void pack_walk(const View& t, uint64_t total) {
+  using Acc = typename AccOf<SDT, DDT>::T;
+  constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
+  const uint64_t nch = (total + C - 1) / C;
+  for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
+    Ent en[U];
+    uint64_t lg[U];
+    bool act[U], full[U];
+    Acc v[U][kVec];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      act[u] = q < total;
+      full[u] = false;
+      if (act[u]) {
+        en[u] = t.resolve(j, q);
+        lg[u] = q - en[u].gstart;
+        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
+        if (full[u]) load8s<SDT, Acc>(en[u].a, lg[u] * kVec, v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      if (full[u]) {
+        store8s<DDT, Acc>(en[u].c, lg[u] * kVec, v[u]);
+      } else {
+        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
+        for (uint64_t i = lg[u] * kVec; i < end; ++i) store1<DDT, Acc>(en[u].c, i, load1<SDT, Acc>(en[u].a, i));
+      }
+    }
+  }
+}
+
+template <int CAP>
+struct PackView {
+  const PackParams<CAP>* p;
+  __device__ __forceinline__ Ent resolve(uint64_t, uint64_t q) const {
+    const int e = find_entry(p->group_start, p->n_entries, q);
+    return Ent{p->src[e], nullptr, p->dst[e], nullptr, p->n[e], p->group_start[e], p->vec_ok[e] != 0};
+  }
+};
+
+constexpr int kPackU = 2;  // groups per thread per chunk: 2 x 32 B in flight per thread (fp32)
+constexpr int kSgdU = 1;   // 3 streams x 32 B in flight per thread already
+
 template <int SDT, int DDT, int CAP>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackParams<CAP> p) {
-  uint64_t g0, g1;
-  cta_range(p.total_groups, g0, g1);
-  if (g0 >= g1) return;
-  int e = find_entry(p.group_start, p.n_entries, g0);
-  for (uint64_t g = g0; g < g1; ++e) {
-    const uint64_t es = p.group_start[e];
-    const uint64_t ee = (e + 1 < p.n_entries) ? p.group_start[e + 1] : p.total_groups;
-    const uint64_t hi = min(g1, ee);
-    pack_segment<SDT, DDT>(p.src[e], p.dst[e], p.n[e], p.vec_ok[e], g - es, hi - es);
-    g = hi;
-  }
+  pack_walk<SDT, DDT, kPackU>(PackView<CAP>{&p}, p.total_groups);
 }
 
 // ------------------------------------------------------------- (b) sum
@@ -356,12 +466,11 @@ template <int DT, int M>
 __global__ void __launch_bounds__(kThreads) sum_kernel(const __grid_constant__ SumParams p) {
   using Acc = typename AccOf<DT, DT>::T;  // f64 -> f64, f32 -> f32, bf16 -> f32
   const int m = (M > 0) ? M : p.m;
-  uint64_t g0, g1;
-  cta_range(p.total_groups, g0, g1);
-  uint64_t q = g0 + threadIdx.x;
-  if (p.vec_ok) {
-    const uint64_t hi_full = min(g1, p.n / kVec);
-    for (; q < hi_full; q += kThreads) {
+  const uint64_t full_groups = p.vec_ok ? p.n / kVec : 0;
+  // chunks of kThreads groups, chunk j to CTA j mod G (see "work split")
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; q < p.total_groups;
+       q += static_cast<uint64_t>(gridDim.x) * kThreads) {
+    if (q < full_groups) {
       const uint64_t i = q * kVec;
       Acc acc[kVec];
       if constexpr (M > 0) {
@@ -384,14 +493,13 @@ __global__ void __launch_bounds__(kThreads) sum_kernel(const __grid_constant__ S
         }
       }
       for (int o = 0; o < p.nout; ++o) store8<DT, Acc>(p.out[o], i, acc);
-    }
-  }
-  for (; q < g1; q += kThreads) {
-    const uint64_t end = min(p.n, (q + 1) * kVec);
-    for (uint64_t j = q * kVec; j < end; ++j) {
-      Acc a = load1<DT, Acc>(p.in[0], j);
-      for (int r = 1; r < m; ++r) a = add_rn(a, load1<DT, Acc>(p.in[r], j));
-      for (int o = 0; o < p.nout; ++o) store1<DT, Acc>(p.out[o], j, a);
+    } else {
+      const uint64_t end = min(p.n, (q + 1) * kVec);
+      for (uint64_t j = q * kVec; j < end; ++j) {
+        Acc a = load1<DT, Acc>(p.in[0], j);
+        for (int r = 1; r < m; ++r) a = add_rn(a, load1<DT, Acc>(p.in[r], j));
+        for (int o = 0; o < p.nout; ++o) store1<DT, Acc>(p.out[o], j, a);
+      }
     }
   }
 }
@@ -477,58 +585,93 @@ __device__ __forceinline__ void sgd_segment(void* w, const void* g, void* mom, u
   }
 }
 
+// Kernel (c) walker: a = g (comm dtype), b = momentum, c = weights.
+template <int WDT, int GDT, bool MOM, int U, typename View>
+__device__ __forceinline__ void sgd_walk(const View& t, uint64_t total, double step_d, double mu_d) {
+  using Acc = typename AccOf<WDT, WDT>::T;  // f64 weights -> f64 math, else f32
+  constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
+  constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
+  const Acc step = static_cast<Acc>(step_d);
+  const Acc mu = static_cast<Acc>(mu_d);
+  const uint64_t nch = (total + C - 1) / C;
+  for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
+    Ent en[U];
+    uint64_t lg[U];
+    bool act[U], full[U];
+    Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      act[u] = q < total;
+      full[u] = false;
+      if (act[u]) {
+        en[u] = t.resolve(j, q);
+        lg[u] = q - en[u].gstart;
+        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
+        if (full[u]) {
+          const uint64_t i = lg[u] * kVec;
+          load8s<GDT, Acc>(en[u].a, i, gv[u]);
+          load8s<WDT, Acc>(en[u].c, i, wv[u]);
+          if constexpr (MOM) load8s<MDT, Acc>(en[u].b, i, mv[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      void* mom = const_cast<void*>(en[u].b);
+      if (full[u]) {
+        const uint64_t i = lg[u] * kVec;
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) sgd_elem<MOM>(wv[u][k], gv[u][k], mv[u][k], step, mu);
+        store8s<WDT, Acc>(en[u].c, i, wv[u]);
+        if constexpr (MOM) store8s<MDT, Acc>(mom, i, mv[u]);
+      } else {
+        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
+        for (uint64_t i = lg[u] * kVec; i < end; ++i) {
+          Acc ww = load1<WDT, Acc>(en[u].c, i), mm = Acc(0);
+          if constexpr (MOM) mm = load1<MDT, Acc>(mom, i);
+          sgd_elem<MOM>(ww, load1<GDT, Acc>(en[u].a, i), mm, step, mu);
+          if constexpr (MOM) store1<MDT, Acc>(mom, i, mm);
+          store1<WDT, Acc>(en[u].c, i, ww);
+        }
+      }
+    }
+  }
+}
+
+template <int CAP>
+struct SgdView {
+  const SgdParams<CAP>* p;
+  __device__ __forceinline__ Ent resolve(uint64_t, uint64_t q) const {
+    const int e = find_entry(p->group_start, p->n_entries, q);
+    return Ent{p->g[e], p->mom[e], p->w[e], nullptr, p->n[e], p->group_start[e], p->vec_ok[e] != 0};
+  }
+};
+
 template <int WDT, int GDT, bool MOM, int CAP>
 __global__ void __launch_bounds__(kThreads) sgd_kernel(const __grid_constant__ SgdParams<CAP> p) {
-  uint64_t g0, g1;
-  cta_range(p.total_groups, g0, g1);
-  if (g0 >= g1) return;
-  int e = find_entry(p.group_start, p.n_entries, g0);
-  for (uint64_t g = g0; g < g1; ++e) {
-    const uint64_t es = p.group_start[e];
-    const uint64_t ee = (e + 1 < p.n_entries) ? p.group_start[e + 1] : p.total_groups;
-    const uint64_t hi = min(g1, ee);
-    sgd_segment<WDT, GDT, MOM>(p.w[e], p.g[e], p.mom[e], p.n[e], p.vec_ok[e], g - es, hi - es,
-                               p.step, p.mu);
-    g = hi;
-  }
+  sgd_walk<WDT, GDT, MOM, kSgdU>(SgdView<CAP>{&p}, p.total_groups, p.step, p.mu);
 }
 
 // ------------------------------------ device-resident tables (buckets)
 
 using DevEntry = DeviceTable::Entry;
 
-// Same even split as the parameter-block kernels; the CTA's first entry was
-// precomputed on the host, so a CTA starts with one dependent L2 load
-// instead of a binary search, and entries are read through L1 (broadcast).
+// The same walkers over a resident table: each chunk's first entry was
+// precomputed on the host (DeviceTable::sync), entries are read through L1.
 template <int SDT, int DDT>
 __global__ void __launch_bounds__(kThreads)
     pack_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
                     const uint8_t* __restrict__ vec, uint64_t total) {
-  uint64_t g0, g1;
-  cta_range(total, g0, g1);
-  if (g0 >= g1) return;
-  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
-    const DevEntry en = tab[e];
-    const uint64_t hi = min(g1, en.gend);
-    pack_segment<SDT, DDT>(en.a, en.c, en.n, vec[e], g0 - en.gstart, hi - en.gstart);
-    g0 = hi;
-  }
+  pack_walk<SDT, DDT, kPackU>(TabView{tab, first, vec}, total);
 }
 
 template <int WDT, int GDT, bool MOM>
 __global__ void __launch_bounds__(kThreads)
     sgd_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
                    const uint8_t* __restrict__ vec, uint64_t total, double step, double mu) {
-  uint64_t g0, g1;
-  cta_range(total, g0, g1);
-  if (g0 >= g1) return;
-  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
-    const DevEntry en = tab[e];
-    const uint64_t hi = min(g1, en.gend);
-    sgd_segment<WDT, GDT, MOM>(en.c, en.a, const_cast<void*>(en.b), en.n, vec[e], g0 - en.gstart,
-                               hi - en.gstart, step, mu);
-    g0 = hi;
-  }
+  sgd_walk<WDT, GDT, MOM, kSgdU>(TabView{tab, first, vec}, total, step, mu);
 }
 
 // (a)+(c) fused for one rank (the allreduce between them is the identity):
@@ -544,64 +687,62 @@ __device__ __forceinline__ Acc comm_cast(Acc x) {
   else return x;
 }
 
-template <int GDT, int CDT, int WDT, bool MOM>
-__device__ __forceinline__ void pack_sgd_segment(const void* g, void* bucket, void* w, void* mom, uint64_t n,
-                                                 bool vec, uint64_t lo, uint64_t hi, double step_d, double mu_d) {
+template <int GDT, int CDT, int WDT, bool MOM, int U>
+__device__ __forceinline__ void pack_sgd_walk(const TabView& t, uint64_t total, double step_d, double mu_d) {
   using Acc = typename AccOf<WDT, WDT>::T;
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
-  constexpr int U = 2;
+  constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
   const Acc step = static_cast<Acc>(step_d);
   const Acc mu = static_cast<Acc>(mu_d);
-  const bool stage = bucket != g;
-  uint64_t q = lo + threadIdx.x;
-  if (vec) {
-    const uint64_t hi_full = min(hi, n / kVec);
-    for (; q + (U - 1) * kThreads < hi_full; q += U * kThreads) {
-      Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
+  const uint64_t nch = (total + C - 1) / C;
+  for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
+    Ent en[U];
+    uint64_t lg[U];
+    bool act[U], full[U];
+    Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = (q + u * kThreads) * kVec;
-        load8<GDT, Acc>(g, i, gv[u]);
-        load8_rw<WDT, Acc>(w, i, wv[u]);
-        if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = (q + u * kThreads) * kVec;
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) gv[u][j] = comm_cast<CDT>(gv[u][j]);
-        if (stage) store8<CDT, Acc>(bucket, i, gv[u]);
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[u][j], gv[u][j], mv[u][j], step, mu);
-        store8<WDT, Acc>(w, i, wv[u]);
-        if constexpr (MOM) store8<MDT, Acc>(mom, i, mv[u]);
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      act[u] = q < total;
+      full[u] = false;
+      if (act[u]) {
+        en[u] = t.resolve(j, q);
+        lg[u] = q - en[u].gstart;
+        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
+        if (full[u]) {
+          const uint64_t i = lg[u] * kVec;
+          load8s<GDT, Acc>(en[u].a, i, gv[u]);
+          load8s<WDT, Acc>(en[u].c, i, wv[u]);
+          if constexpr (MOM) load8s<MDT, Acc>(en[u].b, i, mv[u]);
+        }
       }
     }
-    for (; q < hi_full; q += kThreads) {
-      const uint64_t i = q * kVec;
-      Acc gv[kVec], wv[kVec], mv[kVec];
-      load8<GDT, Acc>(g, i, gv);
-      load8_rw<WDT, Acc>(w, i, wv);
-      if constexpr (MOM) load8_rw<MDT, Acc>(mom, i, mv);
 #pragma unroll
-      for (int j = 0; j < kVec; ++j) gv[j] = comm_cast<CDT>(gv[j]);
-      if (stage) store8<CDT, Acc>(bucket, i, gv);
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      void* mom = const_cast<void*>(en[u].b);
+      const bool stage = en[u].d != en[u].a;
+      if (full[u]) {
+        const uint64_t i = lg[u] * kVec;
 #pragma unroll
-      for (int j = 0; j < kVec; ++j) sgd_elem<MOM>(wv[j], gv[j], mv[j], step, mu);
-      store8<WDT, Acc>(w, i, wv);
-      if constexpr (MOM) store8<MDT, Acc>(mom, i, mv);
-    }
-  }
-  for (; q < hi; q += kThreads) {
-    const uint64_t end = min(n, (q + 1) * kVec);
-    for (uint64_t j = q * kVec; j < end; ++j) {
-      const Acc gg = comm_cast<CDT>(load1<GDT, Acc>(g, j));
-      if (stage) store1<CDT, Acc>(bucket, j, gg);
-      Acc ww = load1<WDT, Acc>(w, j), mm = Acc(0);
-      if constexpr (MOM) mm = load1<MDT, Acc>(mom, j);
-      sgd_elem<MOM>(ww, gg, mm, step, mu);
-      if constexpr (MOM) store1<MDT, Acc>(mom, j, mm);
-      store1<WDT, Acc>(w, j, ww);
+        for (int k = 0; k < kVec; ++k) gv[u][k] = comm_cast<CDT>(gv[u][k]);
+        if (stage) store8s<CDT, Acc>(en[u].d, i, gv[u]);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) sgd_elem<MOM>(wv[u][k], gv[u][k], mv[u][k], step, mu);
+        store8s<WDT, Acc>(en[u].c, i, wv[u]);
+        if constexpr (MOM) store8s<MDT, Acc>(mom, i, mv[u]);
+      } else {
+        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
+        for (uint64_t i = lg[u] * kVec; i < end; ++i) {
+          const Acc gg = comm_cast<CDT>(load1<GDT, Acc>(en[u].a, i));
+          if (stage) store1<CDT, Acc>(en[u].d, i, gg);
+          Acc ww = load1<WDT, Acc>(en[u].c, i), mm = Acc(0);
+          if constexpr (MOM) mm = load1<MDT, Acc>(mom, i);
+          sgd_elem<MOM>(ww, gg, mm, step, mu);
+          if constexpr (MOM) store1<MDT, Acc>(mom, i, mm);
+          store1<WDT, Acc>(en[u].c, i, ww);
+        }
+      }
     }
   }
 }
@@ -610,16 +751,7 @@ template <int GDT, int CDT, int WDT, bool MOM>
 __global__ void __launch_bounds__(kThreads)
     pack_sgd_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
                         const uint8_t* __restrict__ vec, uint64_t total, double step, double mu) {
-  uint64_t g0, g1;
-  cta_range(total, g0, g1);
-  if (g0 >= g1) return;
-  for (int e = first[blockIdx.x]; g0 < g1; ++e) {
-    const DevEntry en = tab[e];
-    const uint64_t hi = min(g1, en.gend);
-    pack_sgd_segment<GDT, CDT, WDT, MOM>(en.a, en.d, en.c, const_cast<void*>(en.b), en.n, vec[e],
-                                         g0 - en.gstart, hi - en.gstart, step, mu);
-    g0 = hi;
-  }
+  pack_sgd_walk<GDT, CDT, WDT, MOM, kSgdU>(TabView{tab, first, vec}, total, step, mu);
 }
 
 // ------------------------- fused NVLink allreduce (+ SGD) over peer memory
@@ -672,7 +804,26 @@ struct P2PParams {
   int sys_fence;  // explicit fence.sc.sys before the release store of a pair barrier (CSB_P2P_FENCE)
   int pack;       // stage the gradients (entry d) into this rank's bucket (entry a) before barrier 0
   uint32_t epoch;
+  uint64_t piece;  // groups per piece of the interleaved CTA map (0: one contiguous range per CTA)
 };
+
+// CTA c's share of shard s: the shard is cut into G x K equal pieces
+// (K ~ L / (G x piece)), piece i to CTA i mod G -- interleaved like the
+// streaming kernels' chunks ("work split": the GPU walks each array front to
+// back), balanced to a group.  The map depends only on (T, N, G, piece),
+// identical on every rank, so CTA c handles the same pieces everywhere --
+// what the per-CTA pair barriers pair.  piece = 0: one contiguous range.
+template <typename F>
+__device__ __forceinline__ void for_pieces(const P2PParams& p, int s, F&& f) {
+  const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
+  const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
+  const uint64_t K = p.piece ? max(static_cast<uint64_t>(1), L / (G * p.piece)) : 1;
+  const uint64_t P = G * K;
+  for (uint64_t k = 0; k < K; ++k) {
+    const uint64_t i = c + k * G;
+    f(s0, s0 + L * i / P, s0 + L * (i + 1) / P);
+  }
+}
 
 __device__ __forceinline__ void flag_store(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -866,12 +1017,8 @@ __device__ __forceinline__ void p2p_pack_range(const P2PParams& p, uint64_t a, u
 
 template <int CDT>
 __device__ __forceinline__ void p2p_pack_column(const P2PParams& p) {
-  const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
-  for (int k = 0; k < p.nranks; ++k) {
-    const int s = (p.rank + k) % p.nranks;  // own shard first
-    const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
-    p2p_pack_range<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
-  }
+  for (int k = 0; k < p.nranks; ++k)  // own shard first
+    for_pieces(p, (p.rank + k) % p.nranks, [&](uint64_t, uint64_t a, uint64_t b) { p2p_pack_range<CDT>(p, a, b); });
 }
 
 // SGD over bucket groups [a, b) of shard `owner` through the entries
@@ -903,20 +1050,16 @@ __device__ __forceinline__ void p2p_update_range(const P2PParams& p, int owner, 
 
 template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
-  const uint64_t T = p.groups;
-  const uint64_t G = gridDim.x, c = blockIdx.x;
   if constexpr (UPDATE && !NVLS) {
     if (p.pack) p2p_pack_column<CDT>(p);
   }
   if (!pair_barrier(p, 0)) return;
-  {
-    const uint64_t s0 = T * p.rank / p.nranks, s1 = T * (p.rank + 1) / p.nranks, L = s1 - s0;
-    if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
-    else p2p_reduce_chunk<CDT, M>(p, s0 + L * c / G, s0 + L * (c + 1) / G);
-  }
+  for_pieces(p, p.rank, [&](uint64_t, uint64_t a, uint64_t b) {
+    if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, a, b);
+    else p2p_reduce_chunk<CDT, M>(p, a, b);
+  });
   auto update_shard = [&](int s) {
-    const uint64_t s0 = T * s / p.nranks, s1 = T * (s + 1) / p.nranks, L = s1 - s0;
-    p2p_update_range<WDT, CDT, MOM>(p, s, s0 + L * c / G, s0 + L * (c + 1) / G);
+    for_pieces(p, s, [&](uint64_t, uint64_t a, uint64_t b) { p2p_update_range<WDT, CDT, MOM>(p, s, a, b); });
   };
   if constexpr (UPDATE && !NVLS) {
     // this CTA just wrote its chunk of the own shard: update it before
@@ -1026,26 +1169,16 @@ __device__ __forceinline__ void zero_gather(const P2PParams& p, int s, uint64_t 
 
 template <int CDT, int WDT, bool MOM, int M>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_constant__ P2PParams p) {
-  const uint64_t T = p.groups;
-  const uint64_t G = gridDim.x, c = blockIdx.x;
-  auto chunk = [&](int s, uint64_t& s0, uint64_t& a, uint64_t& b) {
-    s0 = T * s / p.nranks;
-    const uint64_t L = T * (s + 1) / p.nranks - s0;
-    a = s0 + L * c / G;
-    b = s0 + L * (c + 1) / G;
-  };
-  uint64_t s0, a, b;
   if (p.pack) p2p_pack_column<CDT>(p);
   if (!pair_barrier(p, 0)) return;
-  chunk(p.rank, s0, a, b);
-  zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b);
+  for_pieces(p, p.rank, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b); });
   __syncthreads();
-  zero_gather<WDT>(p, p.rank, s0, a, b);  // own shard: no need to wait for the peers
+  // own shard: no need to wait for the peers
+  for_pieces(p, p.rank, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_gather<WDT>(p, p.rank, s0, a, b); });
   if (!pair_barrier(p, 1)) return;
   for (int k = 1; k < p.nranks; ++k) {
     const int s = (p.rank + k) % p.nranks;
-    chunk(s, s0, a, b);
-    zero_gather<WDT>(p, s, s0, a, b);
+    for_pieces(p, s, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_gather<WDT>(p, s, s0, a, b); });
   }
 }
 
@@ -1197,14 +1330,15 @@ int stream_ctas_per_sm() {
 }
 
 template <typename Kernel>
-int wave_grid(Kernel kernel, uint64_t groups) {
+int wave_grid(Kernel kernel, uint64_t groups, int u = 1) {
   static const int occ = [&] {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess) b = 1;
     return std::max(1, std::min(b, stream_ctas_per_sm()));
   }();
   const uint64_t full = static_cast<uint64_t>(sm_count_for_current_device()) * occ;
-  const uint64_t need = (groups + kThreads - 1) / kThreads;
+  const uint64_t chunk = static_cast<uint64_t>(kThreads) * static_cast<uint64_t>(u);
+  const uint64_t need = (groups + chunk - 1) / chunk;  // chunks: no CTA without one
   return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
 }
 
@@ -1225,7 +1359,7 @@ void launch_pack_typed(const PackParams<CAP>& p, cudaStream_t s) {
   double elems = 0;
   for (int i = 0; i < p.n_entries; ++i) elems += static_cast<double>(p.n[i]);
   LaunchScope ls(kKernPack, elems * (sizeof(typename Elem<SDT>::T) + sizeof(typename Elem<DDT>::T)), s);
-  pack_kernel<SDT, DDT, CAP><<<wave_grid(pack_kernel<SDT, DDT, CAP>, p.total_groups), kThreads, 0, s>>>(p);
+  pack_kernel<SDT, DDT, CAP><<<wave_grid(pack_kernel<SDT, DDT, CAP>, p.total_groups, kPackU), kThreads, 0, s>>>(p);
   check_launch("pack_kernel");
   ls.done();
 }
@@ -1270,7 +1404,7 @@ void launch_sgd_typed(const SgdParams<CAP>& p, cudaStream_t s) {
   const double mom_bytes = MOM ? 2.0 * (WDT == CS_F64 ? 8 : 4) : 0.0;
   LaunchScope ls(kKernSgd,
                  elems * (2.0 * sizeof(typename Elem<WDT>::T) + sizeof(typename Elem<GDT>::T) + mom_bytes), s);
-  sgd_kernel<WDT, GDT, MOM, CAP><<<wave_grid(sgd_kernel<WDT, GDT, MOM, CAP>, p.total_groups), kThreads, 0, s>>>(p);
+  sgd_kernel<WDT, GDT, MOM, CAP><<<wave_grid(sgd_kernel<WDT, GDT, MOM, CAP>, p.total_groups, kSgdU), kThreads, 0, s>>>(p);
   check_launch("sgd_kernel");
   ls.done();
 }
@@ -1451,24 +1585,37 @@ DeviceTable::~DeviceTable() {
   }
 }
 
-// Computes every CTA's first entry for the kernel's one-wave grid and makes
-// the device copy current (uploading only when the bytes differ).
-void DeviceTable::sync(const void* kernel_fn, cudaStream_t s) {
-  (void)kernel_fn;
-  first_.assign(static_cast<size_t>(grid_), 0);
-  size_t e = 0;
-  for (int c = 0; c < grid_; ++c) {
-    const uint64_t g0 = groups_ * static_cast<uint64_t>(c) / static_cast<uint64_t>(grid_);
-    while (e + 1 < host_.size() && host_[e].gend <= g0) ++e;
-    first_[static_cast<size_t>(c)] = static_cast<uint32_t>(e);
+// Computes every chunk's first entry (chunk = kThreads x U groups, see
+// "work split"; first_[nchunks] = the last entry) and makes the device copy
+// current (uploading only when the bytes differ).  chunk_groups = 0: entries
+// only (the peer kernels' tables).
+void DeviceTable::sync(uint64_t chunk_groups, cudaStream_t s) {
+  int dev = 0;
+  CSB_CUDA(cudaGetDevice(&dev));
+  // steady state (same keys every step): nothing to recompute or upload
+  if (dev_ && dev == dev_device_ && chunk_groups == chunk_ && host_.size() == last_host_.size() &&
+      vec_ == last_vec_ &&
+      std::memcmp(host_.data(), last_host_.data(), host_.size() * sizeof(Entry)) == 0)
+    return;
+  last_host_ = host_;
+  last_vec_ = vec_;
+  chunk_ = chunk_groups;
+  first_.clear();
+  if (chunk_groups > 0 && groups_ > 0) {
+    const uint64_t nch = (groups_ + chunk_groups - 1) / chunk_groups;
+    first_.assign(static_cast<size_t>(nch) + 1, 0);
+    size_t e = 0;
+    for (uint64_t j = 0; j <= nch; ++j) {
+      const uint64_t g0 = std::min(j * chunk_groups, groups_ - 1);
+      while (e + 1 < host_.size() && host_[e].gend <= g0) ++e;
+      first_[static_cast<size_t>(j)] = static_cast<uint32_t>(e);
+    }
   }
   const size_t eb = host_.size() * sizeof(Entry), fb = first_.size() * 4, vb = vec_.size();
   std::vector<unsigned char> img(eb + fb + vb);
   std::memcpy(img.data(), host_.data(), eb);
   std::memcpy(img.data() + eb, first_.data(), fb);
   std::memcpy(img.data() + eb + fb, vec_.data(), vb);
-  int dev = 0;
-  CSB_CUDA(cudaGetDevice(&dev));
   if (dev_ && dev == dev_device_ && img == shadow_) return;
   void* fresh = nullptr;
   CSB_CUDA(cudaMallocAsync(&fresh, img.size(), s));
@@ -1502,8 +1649,8 @@ void DeviceTable::pack(const cs_copy_entry* es, int n, int sdt, int ddt, cudaStr
   LaunchScope ls(kKernPack, elems * static_cast<double>(dtype_size(sdt) + dtype_size(ddt)), s);
 #define CSB_PACK_TAB(S, D)                                                              \
   if (sdt == S && ddt == D) {                                                           \
-    grid_ = wave_grid(pack_tab_kernel<S, D>, groups_);                                  \
-    sync(reinterpret_cast<const void*>(pack_tab_kernel<S, D>), s);                      \
+    grid_ = wave_grid(pack_tab_kernel<S, D>, groups_, kPackU);                          \
+    sync(static_cast<uint64_t>(kThreads) * kPackU, s);                                  \
     const char* base = static_cast<const char*>(dev_);                                  \
     pack_tab_kernel<S, D><<<grid_, kThreads, 0, s>>>(                                   \
         reinterpret_cast<const Entry*>(base),                                           \
@@ -1550,8 +1697,8 @@ void DeviceTable::sgd(const cs_update_entry* es, int n, int wdt, int gdt, double
   LaunchScope ls(kKernSgd, elems * (2.0 * dtype_size(wdt) + dtype_size(gdt) + mom_bytes), s);
 #define CSB_SGD_TAB(W, G, M)                                                            \
   if (wdt == W && gdt == G && mom == M) {                                               \
-    grid_ = wave_grid(sgd_tab_kernel<W, G, M>, groups_);                                \
-    sync(reinterpret_cast<const void*>(sgd_tab_kernel<W, G, M>), s);                    \
+    grid_ = wave_grid(sgd_tab_kernel<W, G, M>, groups_, kSgdU);                         \
+    sync(static_cast<uint64_t>(kThreads) * kSgdU, s);                                   \
     const char* base = static_cast<const char*>(dev_);                                  \
     sgd_tab_kernel<W, G, M><<<grid_, kThreads, 0, s>>>(                                 \
         reinterpret_cast<const Entry*>(base),                                           \
@@ -1610,8 +1757,8 @@ void DeviceTable::pack_sgd(const std::vector<PackUpdate>& es, int gdt, int cdt, 
   LaunchScope ls(kKernPackSgd, bytes, s);
 #define CSB_PACK_SGD(G, C, W, M)                                                              \
   if (gdt == G && cdt == C && wdt == W && mom == M) {                                         \
-    grid_ = wave_grid(pack_sgd_tab_kernel<G, C, W, M>, groups_);                              \
-    sync(nullptr, s);                                                                         \
+    grid_ = wave_grid(pack_sgd_tab_kernel<G, C, W, M>, groups_, kSgdU);                       \
+    sync(static_cast<uint64_t>(kThreads) * kSgdU, s);                                         \
     const char* base = static_cast<const char*>(dev_);                                        \
     pack_sgd_tab_kernel<G, C, W, M><<<grid_, kThreads, 0, s>>>(                               \
         reinterpret_cast<const Entry*>(base),                                                 \
@@ -1642,7 +1789,7 @@ const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cu
   grid_ = 0;
   first_.clear();
   if (es.empty()) return nullptr;
-  sync(nullptr, s);
+  sync(0, s);
   return static_cast<const Entry*>(dev_);
 }
 
@@ -1711,6 +1858,11 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   }
   p.mom_b = a.mom_b;
   p.abort_word = a.abort_word;
+  static const uint64_t piece = [] {
+    const char* e = std::getenv("CSB_P2P_PIECE");  // identical on every rank (same environment)
+    return static_cast<uint64_t>(e ? std::max(0, std::atoi(e)) : 512);
+  }();
+  p.piece = piece;
   p.timeout_ns = a.timeout_ns ? a.timeout_ns : p2p_timeout_ns();
   const int grid = p2p_grid(p.groups, a.nranks, a.colocated);
   const bool upd = a.update && a.tab && a.n_entries > 0;

@@ -66,15 +66,18 @@ class DeviceTable {
   const Entry* resident(const std::vector<Entry>& es, cudaStream_t s);
 
  private:
-  void sync(const void* kernel, cudaStream_t s);
+  void sync(uint64_t chunk_groups, cudaStream_t s);
   std::vector<Entry> host_;
-  std::vector<uint32_t> first_;  // first entry of every CTA for grid_
+  std::vector<uint32_t> first_;  // first entry of every chunk (+ the last entry)
   std::vector<uint8_t> vec_;
   uint64_t groups_ = 0;
   int grid_ = 0;
   void* dev_ = nullptr;
   int dev_device_ = -1;
   std::vector<unsigned char> shadow_;  // what dev_ holds
+  std::vector<Entry> last_host_;       // entries / flags / chunk of the last sync
+  std::vector<uint8_t> last_vec_;
+  uint64_t chunk_ = ~0ull;
   uint64_t uploads_ = 0;
 };
 
