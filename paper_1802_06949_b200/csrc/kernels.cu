@@ -345,6 +345,99 @@ __device__ __forceinline__ void store8s(void* base, uint64_t i, const Acc (&v)[k
   }
 }
 
+// E-element slots (one 16-byte vector of the widest dtype a kernel touches):
+// streaming (evict-first), explicitly global loads / stores.
+template <int DT>
+constexpr int elem_bytes() {
+  return DT == CS_F64 ? 8 : (DT == CS_F32 ? 4 : 2);
+}
+
+template <int DT, int E, typename Acc>
+__device__ __forceinline__ void loadE(const void* base, uint64_t i, Acc (&v)[E]) {
+  if constexpr (DT == CS_F64) {
+    static_assert(E == 2 || E == 1, "f64 slots hold 1-2 elements");
+    const double* p = static_cast<const double*>(base) + i;
+    if constexpr (E == 2) {
+      const double2 d = __ldcs(reinterpret_cast<const double2*>(p));
+      v[0] = to_acc<Acc>(d.x);
+      v[1] = to_acc<Acc>(d.y);
+    } else {
+      v[0] = to_acc<Acc>(__ldcs(p));
+    }
+  } else if constexpr (DT == CS_F32) {
+    const float* p = static_cast<const float*>(base) + i;
+    if constexpr (E == 4) {
+      const float4 f = __ldcs(reinterpret_cast<const float4*>(p));
+      v[0] = to_acc<Acc>(f.x);
+      v[1] = to_acc<Acc>(f.y);
+      v[2] = to_acc<Acc>(f.z);
+      v[3] = to_acc<Acc>(f.w);
+    } else {
+      static_assert(E == 2, "f32 slots hold 2 or 4 elements");
+      const float2 f = __ldcs(reinterpret_cast<const float2*>(p));
+      v[0] = to_acc<Acc>(f.x);
+      v[1] = to_acc<Acc>(f.y);
+    }
+  } else {
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + i;
+    uint32_t w[E / 2];
+    if constexpr (E == 8) {
+      const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+      w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+    } else if constexpr (E == 4) {
+      const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
+      w[0] = u.x; w[1] = u.y;
+    } else {
+      static_assert(E == 2, "bf16 slots hold 2, 4 or 8 elements");
+      w[0] = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    }
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+      __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[q]);
+      v[2 * q] = to_acc<Acc>(__low2bfloat16(h));
+      v[2 * q + 1] = to_acc<Acc>(__high2bfloat16(h));
+    }
+  }
+}
+
+template <int DT, int E, typename Acc>
+__device__ __forceinline__ void storeE(void* base, uint64_t i, const Acc (&v)[E]) {
+  if constexpr (DT == CS_F64) {
+    double* p = static_cast<double*>(base) + i;
+    if constexpr (E == 2) __stcs(reinterpret_cast<double2*>(p), make_double2(from_acc<double>(v[0]), from_acc<double>(v[1])));
+    else __stcs(p, from_acc<double>(v[0]));
+  } else if constexpr (DT == CS_F32) {
+    float* p = static_cast<float*>(base) + i;
+    if constexpr (E == 4)
+      __stcs(reinterpret_cast<float4*>(p), make_float4(from_acc<float>(v[0]), from_acc<float>(v[1]),
+                                                       from_acc<float>(v[2]), from_acc<float>(v[3])));
+    else __stcs(reinterpret_cast<float2*>(p), make_float2(from_acc<float>(v[0]), from_acc<float>(v[1])));
+  } else {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + i;
+    uint32_t w[E / 2];
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+      __nv_bfloat162 h = __halves2bfloat162(from_acc<__nv_bfloat16>(v[2 * q]), from_acc<__nv_bfloat16>(v[2 * q + 1]));
+      w[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    if constexpr (E == 8) __stcs(reinterpret_cast<uint4*>(p), make_uint4(w[0], w[1], w[2], w[3]));
+    else if constexpr (E == 4) __stcs(reinterpret_cast<uint2*>(p), make_uint2(w[0], w[1]));
+    else __stcs(reinterpret_cast<unsigned int*>(p), w[0]);
+  }
+}
+
+// Slot geometry of a walk: a chunk of kThreads x U groups is cut into slots
+// of E elements; thread t takes slots t, t + kThreads, ..., so every vector
+// instruction of the CTA covers one contiguous span (a group of 8 per thread
+// -- two 16-B vectors 32 B apart per lane -- measured 8 % slower:
+// tools/streambench.cu group_* vs gridstride_U1).
+template <int... DTS>
+constexpr int slot_elems() {
+  int m = 0;
+  ((m = elem_bytes<DTS>() > m ? elem_bytes<DTS>() : m), ...);
+  return 16 / m;
+}
+
 __device__ __forceinline__ void cta_range(uint64_t T, uint64_t& g0, uint64_t& g1) {
   g0 = T * blockIdx.x / gridDim.x;
   g1 = T * (blockIdx.x + 1) / gridDim.x;
@@ -398,33 +491,38 @@ __device__ __forceinline__ void pack_segment(const void* src, void* dst, uint64_
 template <int SDT, int DDT, int U, typename View>
 __device__ __forceinline__ void pack_walk(const View& t, uint64_t total) {
   using Acc = typename AccOf<SDT, DDT>::T;
+  constexpr int E = slot_elems<SDT, DDT>();
+  constexpr int SPG = kVec / E;  // slots per group
+  constexpr int K = U * SPG;     // slots per thread per chunk
   constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
   const uint64_t nch = (total + C - 1) / C;
   for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
-    Ent en[U];
-    uint64_t lg[U];
-    bool act[U], full[U];
-    Acc v[U][kVec];
+    Ent en[K];
+    uint64_t el[K];
+    bool act[K], full[K];
+    Acc v[K][E];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-      act[u] = q < total;
-      full[u] = false;
-      if (act[u]) {
-        en[u] = t.resolve(j, q);
-        lg[u] = q - en[u].gstart;
-        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
-        if (full[u]) load8s<SDT, Acc>(en[u].a, lg[u] * kVec, v[u]);
+    for (int k = 0; k < K; ++k) {
+      const uint64_t sl = static_cast<uint64_t>(k) * kThreads + threadIdx.x;
+      const uint64_t q = j * C + sl / SPG;
+      act[k] = q < total;
+      full[k] = false;
+      if (act[k]) {
+        en[k] = t.resolve(j, q);
+        el[k] = (q - en[k].gstart) * kVec + (sl % SPG) * E;
+        act[k] = el[k] < en[k].n;
+        full[k] = act[k] && en[k].vec && el[k] + E <= en[k].n;
+        if (full[k]) loadE<SDT, E, Acc>(en[k].a, el[k], v[k]);
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!act[u]) continue;
-      if (full[u]) {
-        store8s<DDT, Acc>(en[u].c, lg[u] * kVec, v[u]);
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      if (full[k]) {
+        storeE<DDT, E, Acc>(en[k].c, el[k], v[k]);
       } else {
-        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
-        for (uint64_t i = lg[u] * kVec; i < end; ++i) store1<DDT, Acc>(en[u].c, i, load1<SDT, Acc>(en[u].a, i));
+        const uint64_t end = min(en[k].n, el[k] + E);
+        for (uint64_t i = el[k]; i < end; ++i) store1<DDT, Acc>(en[k].c, i, load1<SDT, Acc>(en[k].a, i));
       }
     }
   }
@@ -590,50 +688,53 @@ template <int WDT, int GDT, bool MOM, int U, typename View>
 __device__ __forceinline__ void sgd_walk(const View& t, uint64_t total, double step_d, double mu_d) {
   using Acc = typename AccOf<WDT, WDT>::T;  // f64 weights -> f64 math, else f32
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
+  constexpr int E = slot_elems<WDT, GDT, MDT>();
+  constexpr int SPG = kVec / E;
+  constexpr int K = U * SPG;
   constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
   const Acc step = static_cast<Acc>(step_d);
   const Acc mu = static_cast<Acc>(mu_d);
   const uint64_t nch = (total + C - 1) / C;
   for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
-    Ent en[U];
-    uint64_t lg[U];
-    bool act[U], full[U];
-    Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
+    Ent en[K];
+    uint64_t el[K];
+    bool act[K], full[K];
+    Acc gv[K][E], wv[K][E], mv[K][E];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-      act[u] = q < total;
-      full[u] = false;
-      if (act[u]) {
-        en[u] = t.resolve(j, q);
-        lg[u] = q - en[u].gstart;
-        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
-        if (full[u]) {
-          const uint64_t i = lg[u] * kVec;
-          load8s<GDT, Acc>(en[u].a, i, gv[u]);
-          load8s<WDT, Acc>(en[u].c, i, wv[u]);
-          if constexpr (MOM) load8s<MDT, Acc>(en[u].b, i, mv[u]);
+    for (int k = 0; k < K; ++k) {
+      const uint64_t sl = static_cast<uint64_t>(k) * kThreads + threadIdx.x;
+      const uint64_t q = j * C + sl / SPG;
+      act[k] = q < total;
+      full[k] = false;
+      if (act[k]) {
+        en[k] = t.resolve(j, q);
+        el[k] = (q - en[k].gstart) * kVec + (sl % SPG) * E;
+        act[k] = el[k] < en[k].n;
+        full[k] = act[k] && en[k].vec && el[k] + E <= en[k].n;
+        if (full[k]) {
+          loadE<GDT, E, Acc>(en[k].a, el[k], gv[k]);
+          loadE<WDT, E, Acc>(en[k].c, el[k], wv[k]);
+          if constexpr (MOM) loadE<MDT, E, Acc>(en[k].b, el[k], mv[k]);
         }
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!act[u]) continue;
-      void* mom = const_cast<void*>(en[u].b);
-      if (full[u]) {
-        const uint64_t i = lg[u] * kVec;
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      void* mom = const_cast<void*>(en[k].b);
+      if (full[k]) {
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) sgd_elem<MOM>(wv[u][k], gv[u][k], mv[u][k], step, mu);
-        store8s<WDT, Acc>(en[u].c, i, wv[u]);
-        if constexpr (MOM) store8s<MDT, Acc>(mom, i, mv[u]);
+        for (int x = 0; x < E; ++x) sgd_elem<MOM>(wv[k][x], gv[k][x], mv[k][x], step, mu);
+        storeE<WDT, E, Acc>(en[k].c, el[k], wv[k]);
+        if constexpr (MOM) storeE<MDT, E, Acc>(mom, el[k], mv[k]);
       } else {
-        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
-        for (uint64_t i = lg[u] * kVec; i < end; ++i) {
-          Acc ww = load1<WDT, Acc>(en[u].c, i), mm = Acc(0);
+        const uint64_t end = min(en[k].n, el[k] + E);
+        for (uint64_t i = el[k]; i < end; ++i) {
+          Acc ww = load1<WDT, Acc>(en[k].c, i), mm = Acc(0);
           if constexpr (MOM) mm = load1<MDT, Acc>(mom, i);
-          sgd_elem<MOM>(ww, load1<GDT, Acc>(en[u].a, i), mm, step, mu);
+          sgd_elem<MOM>(ww, load1<GDT, Acc>(en[k].a, i), mm, step, mu);
           if constexpr (MOM) store1<MDT, Acc>(mom, i, mm);
-          store1<WDT, Acc>(en[u].c, i, ww);
+          store1<WDT, Acc>(en[k].c, i, ww);
         }
       }
     }
@@ -691,56 +792,59 @@ template <int GDT, int CDT, int WDT, bool MOM, int U>
 __device__ __forceinline__ void pack_sgd_walk(const TabView& t, uint64_t total, double step_d, double mu_d) {
   using Acc = typename AccOf<WDT, WDT>::T;
   constexpr int MDT = (WDT == CS_F64) ? CS_F64 : CS_F32;
+  constexpr int E = slot_elems<GDT, CDT, WDT, MDT>();
+  constexpr int SPG = kVec / E;
+  constexpr int K = U * SPG;
   constexpr uint64_t C = static_cast<uint64_t>(kThreads) * U;
   const Acc step = static_cast<Acc>(step_d);
   const Acc mu = static_cast<Acc>(mu_d);
   const uint64_t nch = (total + C - 1) / C;
   for (uint64_t j = blockIdx.x; j < nch; j += gridDim.x) {
-    Ent en[U];
-    uint64_t lg[U];
-    bool act[U], full[U];
-    Acc gv[U][kVec], wv[U][kVec], mv[U][kVec];
+    Ent en[K];
+    uint64_t el[K];
+    bool act[K], full[K];
+    Acc gv[K][E], wv[K][E], mv[K][E];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t q = j * C + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-      act[u] = q < total;
-      full[u] = false;
-      if (act[u]) {
-        en[u] = t.resolve(j, q);
-        lg[u] = q - en[u].gstart;
-        full[u] = en[u].vec && (lg[u] + 1) * kVec <= en[u].n;
-        if (full[u]) {
-          const uint64_t i = lg[u] * kVec;
-          load8s<GDT, Acc>(en[u].a, i, gv[u]);
-          load8s<WDT, Acc>(en[u].c, i, wv[u]);
-          if constexpr (MOM) load8s<MDT, Acc>(en[u].b, i, mv[u]);
+    for (int k = 0; k < K; ++k) {
+      const uint64_t sl = static_cast<uint64_t>(k) * kThreads + threadIdx.x;
+      const uint64_t q = j * C + sl / SPG;
+      act[k] = q < total;
+      full[k] = false;
+      if (act[k]) {
+        en[k] = t.resolve(j, q);
+        el[k] = (q - en[k].gstart) * kVec + (sl % SPG) * E;
+        act[k] = el[k] < en[k].n;
+        full[k] = act[k] && en[k].vec && el[k] + E <= en[k].n;
+        if (full[k]) {
+          loadE<GDT, E, Acc>(en[k].a, el[k], gv[k]);
+          loadE<WDT, E, Acc>(en[k].c, el[k], wv[k]);
+          if constexpr (MOM) loadE<MDT, E, Acc>(en[k].b, el[k], mv[k]);
         }
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!act[u]) continue;
-      void* mom = const_cast<void*>(en[u].b);
-      const bool stage = en[u].d != en[u].a;
-      if (full[u]) {
-        const uint64_t i = lg[u] * kVec;
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      void* mom = const_cast<void*>(en[k].b);
+      const bool stage = en[k].d != en[k].a;
+      if (full[k]) {
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) gv[u][k] = comm_cast<CDT>(gv[u][k]);
-        if (stage) store8s<CDT, Acc>(en[u].d, i, gv[u]);
+        for (int x = 0; x < E; ++x) gv[k][x] = comm_cast<CDT>(gv[k][x]);
+        if (stage) storeE<CDT, E, Acc>(en[k].d, el[k], gv[k]);
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) sgd_elem<MOM>(wv[u][k], gv[u][k], mv[u][k], step, mu);
-        store8s<WDT, Acc>(en[u].c, i, wv[u]);
-        if constexpr (MOM) store8s<MDT, Acc>(mom, i, mv[u]);
+        for (int x = 0; x < E; ++x) sgd_elem<MOM>(wv[k][x], gv[k][x], mv[k][x], step, mu);
+        storeE<WDT, E, Acc>(en[k].c, el[k], wv[k]);
+        if constexpr (MOM) storeE<MDT, E, Acc>(mom, el[k], mv[k]);
       } else {
-        const uint64_t end = min(en[u].n, (lg[u] + 1) * kVec);
-        for (uint64_t i = lg[u] * kVec; i < end; ++i) {
-          const Acc gg = comm_cast<CDT>(load1<GDT, Acc>(en[u].a, i));
-          if (stage) store1<CDT, Acc>(en[u].d, i, gg);
-          Acc ww = load1<WDT, Acc>(en[u].c, i), mm = Acc(0);
+        const uint64_t end = min(en[k].n, el[k] + E);
+        for (uint64_t i = el[k]; i < end; ++i) {
+          const Acc gg = comm_cast<CDT>(load1<GDT, Acc>(en[k].a, i));
+          if (stage) store1<CDT, Acc>(en[k].d, i, gg);
+          Acc ww = load1<WDT, Acc>(en[k].c, i), mm = Acc(0);
           if constexpr (MOM) mm = load1<MDT, Acc>(mom, i);
           sgd_elem<MOM>(ww, gg, mm, step, mu);
           if constexpr (MOM) store1<MDT, Acc>(mom, i, mm);
-          store1<WDT, Acc>(en[u].c, i, ww);
+          store1<WDT, Acc>(en[k].c, i, ww);
         }
       }
     }
