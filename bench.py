@@ -386,6 +386,8 @@ def parity_check(api, engine, transport, rank, world, keys, kw, comms, gdt, step
         out = {"steps": steps, "ranks": world, "keys_checked": len(sel), "elems_checked": int(w.size),
                "bit_exact_vs_restatement": bool(np.array_equal(w, exp)),
                "max_rel_err_vs_f64": err, "tolerance": tol, "within_tolerance": err <= tol,
+               "rel_err_scale": "|w0| + lr*rescale*C*sum_r|g_r| per element, C = the gradient's total "
+                                "coefficient over the steps (SURVEY 8(c)'s update scale, over T momentum steps)",
                "ranks_agree": agree,
                "oracle": f"oracle/oracle.c or_synth_expect ({wname} weights, {cname} sums in rank order; "
                          f"pinned to the reference's golden weights), {time.time() - t0:.1f} s on the host"}
