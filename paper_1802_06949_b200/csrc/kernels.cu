@@ -916,7 +916,10 @@ struct P2PParams {
 // streaming kernels' chunks ("work split": the GPU walks each array front to
 // back), balanced to a group.  The map depends only on (T, N, G, piece),
 // identical on every rank, so CTA c handles the same pieces everywhere --
-// what the per-CTA pair barriers pair.  piece = 0: one contiguous range.
+// what the per-CTA pair barriers pair.  piece = 0 (the default): one
+// contiguous range per CTA -- for these NVLink-bound kernels the interleaved
+// map measured slower (ResNet-50 at 4 GPUs: 0.427 vs 0.340 ms/step with
+// CSB_P2P_PIECE=512), unlike the HBM-bound streaming kernels.
 template <typename F>
 __device__ __forceinline__ void for_pieces(const P2PParams& p, int s, F&& f) {
   const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
@@ -1089,6 +1092,10 @@ __device__ __forceinline__ void nvls_reduce_chunk(const P2PParams& p, uint64_t a
     ld(v, r);
     st(v, r);
   }
+  // the sums were written through the multicast VA and are read back through
+  // the unicast one after the pair barrier: virtually aliased accesses need a
+  // proxy fence on both sides (the consumer side is after barrier 1)
+  asm volatile("fence.proxy.alias;" ::: "memory");
 }
 
 // Kernel (a) folded into the peer kernels' phase 0.  CTA c stages column c
@@ -1172,6 +1179,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __g
     update_shard(p.rank);
   }
   if (!pair_barrier(p, 1)) return;
+  if constexpr (NVLS) asm volatile("fence.proxy.alias;" ::: "memory");
   if constexpr (UPDATE) {
     // the other shards, staggered so the ranks start on different owners
     for (int k = NVLS ? 0 : 1; k < p.nranks; ++k) update_shard((p.rank + k) % p.nranks);
@@ -1964,7 +1972,7 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   p.abort_word = a.abort_word;
   static const uint64_t piece = [] {
     const char* e = std::getenv("CSB_P2P_PIECE");  // identical on every rank (same environment)
-    return static_cast<uint64_t>(e ? std::max(0, std::atoi(e)) : 512);
+    return static_cast<uint64_t>(e ? std::max(0, std::atoi(e)) : 0);
   }();
   p.piece = piece;
   p.timeout_ns = a.timeout_ns ? a.timeout_ns : p2p_timeout_ns();

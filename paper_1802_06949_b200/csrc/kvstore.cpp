@@ -634,7 +634,10 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         }
         std::vector<Tag> p2p_reads;
         if (fuse_p2p) {
-          p2p_reads = B.deferred_reads;
+          // the pushed gradients; bucket views are already among the writes
+          for (const Tag& t : B.deferred_reads)
+            if (std::none_of(B.view_tags.begin(), B.view_tags.end(), [&](const Tag& v) { return v.id == t.id; }))
+              p2p_reads.push_back(t);
           B.deferred.clear();
           B.deferred_reads.clear();
           B.deferred_dt = -1;
@@ -689,7 +692,10 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
           if (dk == k) g = e.src;
         pu.push_back(DeviceTable::PackUpdate{g, key_ptr(k), o.data, keys_[static_cast<size_t>(k)].mom, o.numel});
       }
-      std::vector<Tag> reads = B.deferred_reads;
+      std::vector<Tag> reads;
+      for (const Tag& t : B.deferred_reads)
+        if (std::none_of(B.view_tags.begin(), B.view_tags.end(), [&](const Tag& v) { return v.id == t.id; }))
+          reads.push_back(t);
       for (const Tag& t : B.view_tags) reads.push_back(t);
       std::vector<Tag> fmuts{B.tag};
       for (const Tag& t : out_tags) fmuts.push_back(t);

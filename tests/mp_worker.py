@@ -312,3 +312,7 @@ def run_colocated(case, world, outdir, watchdog_ms=60000):
     if errs:
         raise errs[0]
     return outs
+
+
+if __name__ == "__main__":
+    main()
