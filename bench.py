@@ -219,7 +219,7 @@ class Clocks:
 
 
 # committed `ncu --set full` captures of the N=1 headline workload, newest first
-NCU_CAPTURES = ["r2", "r1b"]
+NCU_CAPTURES = ("r2", "r1b")  # newest first
 
 
 def ncu_traffic(kernel: str):
