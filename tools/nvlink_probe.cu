@@ -250,9 +250,75 @@ int main(int argc, char** argv) {
       run("pullred_u2", pullred_k<2>, grid, block, 0, inbound);
     }
   }
-  for (int grid : {148, 296, 592}) {
-    run("bulk_16k_s4", bulk_k<16384, 4>, grid, 32, 4 * 16384, inbound);
-    run("bulk_8k_s8", bulk_k<8192, 8>, grid, 32, 8 * 8192, inbound);
+  if (!(argc > 3 && atoi(argv[3]) == 1)) {
+    for (int grid : {148, 296, 592}) {
+      run("bulk_16k_s4", bulk_k<16384, 4>, grid, 32, 4 * 16384, inbound);
+      run("bulk_8k_s8", bulk_k<8192, 8>, grid, 32, 8 * 8192, inbound);
+    }
   }
+  // Copy engines: the same all-to-all exchange through cudaMemcpyPeerAsync
+  // (no SM involved).  pull = the destination GPU's stream issues the copy,
+  // push = the source GPU's; "1s" = one stream per GPU (copies serialise),
+  // "ps" = one stream per peer (copies run concurrently on several CEs);
+  // "oneway" = GPU 0 pulls from GPU 1 only (the 770 GB/s reference figure).
+  std::vector<std::vector<cudaStream_t>> ps(n, std::vector<cudaStream_t>(kMax));
+  std::vector<std::vector<cudaEvent_t>> pe(n, std::vector<cudaEvent_t>(kMax));
+  for (int g = 0; g < n; ++g) {
+    CK(cudaSetDevice(g));
+    for (int k = 0; k < kMax; ++k) {
+      CK(cudaStreamCreateWithFlags(&ps[g][k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&pe[g][k], cudaEventDisableTiming));
+    }
+  }
+  const uint64_t Tb = bytes / n;
+  auto run_ce = [&](const char* name, bool push, bool par, bool oneway) {
+    const int iters = 20;
+    for (int rep = 0; rep < 2; ++rep) {
+      for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaDeviceSynchronize());
+      }
+      for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventRecord(e0[g], st[g]));
+        for (int k = 1; k < n; ++k) CK(cudaStreamWaitEvent(ps[g][k], e0[g], 0));
+        for (int i = 0; i < (rep ? iters : 3); ++i) {
+          for (int k = 1; k < n; ++k) {
+            if (oneway && (g != 0 || k != 1)) continue;
+            cudaStream_t cs = par ? ps[g][k] : st[g];
+            const int p = (g + k) % n;
+            if (!push) CK(cudaMemcpyPeerAsync(reinterpret_cast<char*>(s[g]) + p * Tb, g,
+                                              reinterpret_cast<char*>(b[p]) + g * Tb, p, Tb, cs));
+            else CK(cudaMemcpyPeerAsync(reinterpret_cast<char*>(s[p]) + g * Tb, p,
+                                        reinterpret_cast<char*>(b[g]) + p * Tb, g, Tb, cs));
+          }
+        }
+        if (par)
+          for (int k = 1; k < n; ++k) {
+            CK(cudaEventRecord(pe[g][k], ps[g][k]));
+            CK(cudaStreamWaitEvent(st[g], pe[g][k], 0));
+          }
+        CK(cudaEventRecord(e1[g], st[g]));
+      }
+      float worst = 0;
+      for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventSynchronize(e1[g]));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+        worst = ms > worst ? ms : worst;
+      }
+      if (rep) {
+        const double us = 1000.0 * worst / iters;
+        const double lb = oneway ? static_cast<double>(Tb) : inbound;
+        printf("{\"pattern\": \"%s\", \"us\": %.2f, \"link_GBps_per_dir\": %.1f}\n", name, us, lb / (us * 1e3));
+      }
+    }
+  };
+  run_ce("ce_pull_oneway", false, false, true);
+  run_ce("ce_pull_1s", false, false, false);
+  run_ce("ce_pull_ps", false, true, false);
+  run_ce("ce_push_1s", true, false, false);
+  run_ce("ce_push_ps", true, true, false);
   return 0;
 }
