@@ -112,6 +112,9 @@ def parse():
                         "fp32 gradients: sharded master weights + momentum, weight all-gather, bit-identical "
                         "results; bf16 gradient sets keep the replicated update, whose all-gather moves bf16 "
                         "sums instead of fp32 weights)")
+    p.add_argument("--no-direct", dest="direct", action="store_false",
+                   help="N>1, fused peer kernel: stage the gradients into the comm buckets (kvstore.cpp:109) "
+                        "instead of registering the gradient arena and reading every rank's gradients in place")
     p.add_argument("--grad-views", action="store_true",
                    help="gradients produced in place in the comm buckets (gradient-as-bucket-view): "
                         "push copies nothing")
@@ -260,6 +263,13 @@ def workload(args):
     return keyset, mode, outstanding, dtype, bucket_mb, bwd_spec
 
 
+def direct_active(args, mode, bucket_mb, world) -> bool:
+    """In-place peer reads of registered gradients: N>1, the fused peer
+    kernel (DepCha / Funnel over fusion buckets), separate gradient tensors."""
+    return (world > 1 and args.direct and not args.grad_views and mode != "concom" and bool(bucket_mb)
+            and args.comm in (None, "p2p"))
+
+
 def config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world) -> dict:
     """The workload, identical in both arms (the driver compares them)."""
     return {"workload": f"{args.config}-{mode}", "keys": len(keys), "params": sum(keys), "mode": mode,
@@ -268,7 +278,10 @@ def config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world) -> dict:
             "l2": "inputs larger than L2 (no flush)",
             "producer_order": "per-rank random (seeded)" if args.config == "stress" else "reverse key order",
             "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
-            else "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)",
+            else ("separate gradient tensors in one registered region (KvStore.register_grads): the fused "
+                  "kernel reads every rank's gradients in place over NVLink, nothing staged"
+                  if direct_active(args, mode, bucket_mb, world) else
+                  "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"),
             "step": "push + allreduce + pull/SGD update over every key (trainer.cpp:112-141), no backward",
             "value_basis": f"gradient bytes per rank = params x {ELEM[dtype]} B ({dtype}) per step time, per GPU"}
 
@@ -395,6 +408,55 @@ def parity_check(api, engine, transport, rank, world, keys, kw, comms, gdt, step
     return out
 
 
+# ------------------------------------------------------------------ busbw
+
+def busbw_sweep(api, transport, rank, world, max_over_ranks, sizes_mb=(16, 64, 256), iters=20):
+    """Bus bandwidth (nccl-tests convention: algbw x 2(N-1)/N) of one fp32
+    bucket allreduce per size: the peer-memory kernel alone (rank-order
+    sums, no update), the same fused with the SGD / momentum update of the
+    whole bucket, and NCCL's allreduce.  CUDA events on the launch stream,
+    max over ranks.  Peak: the measured peer copy (770 GB/s per direction);
+    `ceiling_gbs` is the all-to-all NVLink ceiling tools/nvlink_probe.cu
+    measures with every GPU sending and receiving at once."""
+    import torch
+    out = {"unit": "GB/s", "peak": peaks().get("nvlink_gbs_per_dir", 770.0),
+           "ceiling_gbs": {2: 692.5, 4: 581.2}.get(world),
+           "ceiling_source": "profiles/r2_nvlink_probe_n%d.txt best all-to-all pattern" % world,
+           "sizes": {}}
+    s = torch.cuda.Stream()
+    sh = s.cuda_stream
+    for mb in sizes_mb:
+        n = int(mb * 2**20 / 4) // 64 * 64
+        buf = torch.randn(n, device="cuda")
+        w = torch.randn(n, device="cuda")
+        m = torch.zeros(n, device="cuda")
+        peers = transport.share_buffer(buf.data_ptr())
+        upd = ([(w.data_ptr(), buf.data_ptr(), m.data_ptr(), n)], api.F32, 0.1, 1e-3, 0.9)
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(iters):
+                fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            return max_over_ranks(e0.elapsed_time(e1) / iters) * 1000.0  # us
+
+        r = {}
+        for name, fn in (("p2p", lambda: transport.allreduce_p2p(0, rank, peers, n, api.F32, 0, None, sh)),
+                         ("p2p_fused_sgd", lambda: transport.allreduce_p2p(0, rank, peers, n, api.F32, 0, upd, sh)),
+                         ("nccl", lambda: transport.allreduce_sum(0, rank, buf, 0, sh))):
+            us = timed(fn)
+            bw = 4 * n * 2 * (world - 1) / world / (us * 1e3)
+            r[name] = {"us": round(us, 2), "busbw": round(bw, 1), "frac": round(bw / out["peak"], 4)}
+        out["sizes"][f"{mb}MiB"] = r
+        del buf, w, m
+    return out
+
+
 # ------------------------------------------------------------------ ours
 
 def main():
@@ -448,14 +510,15 @@ def main():
     comms_par = api.create_communicators(transport, outstanding) if (concom and args.parity) else []
     sched_outstanding = 4
     comms_sched = (api.create_communicators(transport, sched_outstanding)
-                   if (world > 1 and not args.no_extras and not concom) else [])
+                   if (not args.no_extras and not concom) else [])
     engine = api.Engine(args.engine_threads, rank, None, local_rank)
     common = dict(mode=mode, w_dtype=api.F32, g_dtype=dt, comm_dtype=dt,
                   bucket_bytes=int(bucket_mb * 2**20), issue_order=1 if args.issue_order == "descending" else 0,
                   outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * world), momentum=args.momentum,
                   backward_ns=int(bwd_ms * 1e6), comm_priority=-5,
                   p2p={"nccl": 0, "p2p": 1, "nvls": 2}[args.comm], grad_views=args.grad_views,
-                  zero=zero_on, order_seed=1 if args.config == "stress" else 0)
+                  zero=zero_on, order_seed=1 if args.config == "stress" else 0,
+                  direct_grads=direct_active(args, mode, bucket_mb, world))
     path = {"collectives": ("identity (1 rank)" if world == 1 else
                             {"nccl": "NCCL" + (f", {outstanding} concurrent communicators" if concom else ""),
                              "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
@@ -573,33 +636,37 @@ def main():
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}
                                         for k, v in kstats.items()}}
 
-        # ---- the paper's three schedules on the same gradient set (N>1)
-        if world > 1:
-            scheds = {mode: {"value": line["value"], "ms_per_step": line["ms_per_step"],
-                             "collectives": path["collectives"]}}
-            for sched in ("funnel", "depcha", "concom"):
-                if sched in scheds:
+        # ---- the paper's three schedules on the same gradient set
+        scheds = {mode: {"value": line["value"], "ms_per_step": line["ms_per_step"],
+                         "collectives": path["collectives"]}}
+        for sched in ("funnel", "depcha", "concom"):
+            if sched in scheds:
+                continue
+            if sched == "concom":
+                if not comms_sched:
                     continue
-                if sched == "concom":
-                    if not comms_sched:
-                        continue
-                    kw = {**common, "mode": "concom", "outstanding": sched_outstanding, "p2p": 0, "zero": False,
-                          "bucket_bytes": 25 << 20}
-                    coll = f"NCCL, {sched_outstanding} communicators, 25 MiB buckets"
-                    cc = comms_sched
-                else:
-                    kw = {**common, "mode": sched, "zero": common["zero"] and sched == "depcha"}
-                    coll = path["collectives"]
-                    cc = []
-                ms_s = api.SynthModel(engine, transport, rank, world, keys, concom_comms=cc, **kw)
-                ms_s.init()
-                ms_s.run(args.warmup, COMM)
-                barrier()
-                t_s = max_over_ranks(ms_s.run(args.steps, COMM)) / args.steps
-                scheds[sched] = {"value": round(gbytes / (t_s * 1e6), 3), "ms_per_step": round(t_s, 4),
-                                 "collectives": coll}
-                ms_s.close()
-            line["schedules"] = scheds
+                kw = {**common, "mode": "concom", "outstanding": sched_outstanding, "p2p": 0, "zero": False,
+                      "bucket_bytes": 25 << 20}
+                coll = (f"NCCL, {sched_outstanding} communicators, 25 MiB buckets" if world > 1 else
+                        f"identity (1 rank), {sched_outstanding} communicators, 25 MiB buckets")
+                cc = comms_sched
+            else:
+                kw = {**common, "mode": sched, "zero": common["zero"] and sched == "depcha"}
+                coll = path["collectives"]
+                cc = []
+            ms_s = api.SynthModel(engine, transport, rank, world, keys, concom_comms=cc, **kw)
+            ms_s.init()
+            ms_s.run(args.warmup, COMM)
+            barrier()
+            t_s = max_over_ranks(ms_s.run(args.steps, COMM)) / args.steps
+            scheds[sched] = {"value": round(gbytes / (t_s * 1e6), 3), "ms_per_step": round(t_s, 4),
+                             "collectives": coll}
+            ms_s.close()
+        line["schedules"] = scheds
+
+        # ---- allreduce bus bandwidth per bucket size (N>1)
+        if world > 1:
+            line["allreduce_busbw"] = busbw_sweep(api, transport, rank, world, max_over_ranks)
 
         # ---- the same aggregation with gradient-as-bucket-view (no pack copy)
         if not args.grad_views and bucket_mb > 0:

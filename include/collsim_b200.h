@@ -275,6 +275,14 @@ int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems)
  * cs_kv_arena: the one allocation holding every fusion bucket (to zero it). */
 int cs_kv_bucket_view(cs_kvstore_t kv, int key, void** ptr);
 int cs_kv_arena(cs_kvstore_t kv, void** base, uint64_t* bytes);
+/* Setup collective (every rank, same order; peer-memory path only, a no-op
+ * otherwise): the allocation holding this rank's gradients -- a cudaMalloc
+ * base, keys at the same offsets on every rank.  A whole-bucket
+ * cs_kv_pull_update whose pushed gradients all lie inside it makes the fused
+ * peer kernel read every rank's gradients in place (nothing is staged into
+ * the buckets; replaces the kvstore.cpp:109 copy).  Ranks whose layouts
+ * differ fail with CS_ERR_MISMATCH before any launch. */
+int cs_kv_register_grads(cs_kvstore_t kv, void* base, uint64_t bytes);
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
 int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);
 
@@ -299,6 +307,8 @@ typedef struct cs_synth_config {
   int zero;               /* as cs_kv_config.zero */
   int order_seed;         /* != 0: this rank's gradients become ready in a random order (seeded per
                              rank) -- the deadlock-stress producer of SURVEY §8d config 5 */
+  int direct_grads;       /* 1: the gradient arena is registered (cs_kv_register_grads): at N > 1 the
+                             fused peer kernel reads every rank's gradients in place, no staging */
 } cs_synth_config;
 enum { CS_STEP_BACKWARD = 1, CS_STEP_COMM = 2, CS_STEP_LOCAL_UPDATE = 4, CS_STEP_CHECKSUM = 8 };
 int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const cs_synth_config* cfg,

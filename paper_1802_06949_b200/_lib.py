@@ -124,6 +124,7 @@ SIGNATURES = {
     "cs_kv_key_map": [_P, _I, _PI, _PU64],
     "cs_kv_bucket_view": [_P, _I, C.POINTER(_P)],
     "cs_kv_arena": [_P, C.POINTER(_P), _PU64],
+    "cs_kv_register_grads": [_P, _P, C.c_uint64],
     "cs_kv_num_buckets": [_P, _PI],
     "cs_kv_bucket_lane": [_P, _I, _PI],
     "cs_synth_create": [_P, _P, _I, _I, C.c_void_p, _PU64, _I, _PI, _I, C.POINTER(_P)],
@@ -152,7 +153,8 @@ class SynthConfigC(C.Structure):
                 ("lr", C.c_double), ("rescale", C.c_double), ("momentum", C.c_double),
                 ("backward_ns", C.c_uint64), ("backward_ctas", C.c_int), ("fused_update", C.c_int),
                 ("comm_priority", C.c_int), ("host_source", C.c_int), ("p2p", C.c_int),
-                ("grad_views", C.c_int), ("zero", C.c_int), ("order_seed", C.c_int)]
+                ("grad_views", C.c_int), ("zero", C.c_int), ("order_seed", C.c_int),
+                ("direct_grads", C.c_int)]
 
 
 CS_STEP_BACKWARD, CS_STEP_COMM, CS_STEP_LOCAL_UPDATE, CS_STEP_CHECKSUM = 1, 2, 4, 8

@@ -538,6 +538,12 @@ class KvStore:
         comm dtype): produce the gradient into it and push it as the key's slot."""
         return device_tensor(self.bucket_view(key), numel, dtype, device)
 
+    def register_grads(self, base: int, nbytes: int) -> None:
+        """Setup collective: the allocation holding this rank's gradients
+        (cudaMalloc base, same layout on every rank); whole-bucket
+        pull_updates then read every rank's gradients in place (N > 1)."""
+        check(lib.cs_kv_register_grads(self.h, base, nbytes))
+
     def arena(self) -> tuple[int, int]:
         p, n = C.c_void_p(), C.c_uint64()
         check(lib.cs_kv_arena(self.h, C.byref(p), C.byref(n)))
@@ -607,11 +613,11 @@ class SynthModel:
                  backward_ctas: int = 0, fused_update: bool = True, comm_priority: int = 0, p2p: bool = False,
                  host_source: bool = False, concom_comms: Sequence[int] = (),
                  ready_ms: Sequence[float] | None = None, grad_views: bool = False, zero: bool = False,
-                 order_seed: int = 0):
+                 order_seed: int = 0, direct_grads: bool = False):
         cfg = _lib.SynthConfigC(MODES[mode], w_dtype, g_dtype, comm_dtype, bucket_bytes, issue_order,
                                 outstanding, lr, rescale, momentum, backward_ns, backward_ctas,
                                 int(fused_update), comm_priority, int(host_source), int(p2p), int(grad_views),
-                                int(zero), int(order_seed))
+                                int(zero), int(order_seed), int(direct_grads))
         sz = (C.c_uint64 * len(sizes))(*sizes)
         comms = (C.c_int * max(1, len(concom_comms)))(*concom_comms)
         h = C.c_void_p()

@@ -602,6 +602,12 @@ int cs_kv_arena(cs_kvstore_t kv, void** base, uint64_t* bytes) {
     kv->kv->arena(base, bytes);
   });
 }
+int cs_kv_register_grads(cs_kvstore_t kv, void* base, uint64_t bytes) {
+  return guard([&] {
+    CHECK_HANDLE(kv);
+    kv->kv->register_grads(base, bytes);
+  });
+}
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out) {
   return guard([&] {
     CHECK_HANDLE(kv);
@@ -646,6 +652,7 @@ int cs_synth_create(cs_engine_t e, cs_transport_t t, int rank, int nranks, const
     c.grad_views = cfg->grad_views != 0;
     c.zero = cfg->zero;
     c.order_seed = cfg->order_seed;
+    c.direct_grads = cfg->direct_grads != 0;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);
@@ -683,6 +690,7 @@ int cs_synth_create_profiled(cs_engine_t e, cs_transport_t t, int rank, int nran
     c.grad_views = cfg->grad_views != 0;
     c.zero = cfg->zero;
     c.order_seed = cfg->order_seed;
+    c.direct_grads = cfg->direct_grads != 0;
     std::vector<int> comms(concom_comms, concom_comms + std::max(0, n_comms));
     auto h = std::make_unique<cs_synth>();
     h->m = std::make_unique<SynthModel>(*e->e, *t->t, rank, nranks, c, comms);

@@ -54,6 +54,7 @@ Engine::Engine(int num_worker_threads, int rank, TraceSink* trace, int device)
   pool_->device = device;
   if (const char* s = std::getenv("CSB_ENGINE_SPIN_US")) spin_ = std::chrono::microseconds(std::atoll(s));
   lanes_.reserve(kMaxLanes);
+  lane_seq_.assign(kMaxLanes, 0);
   if (device_ >= 0) {
     int count = 0;
     CSB_CUDA(cudaGetDeviceCount(&count));
@@ -287,6 +288,17 @@ void Engine::complete(Operation* op, EventRef done, std::exception_ptr failure) 
   control_cv_.notify_all();
 }
 
+std::vector<const EventObj*> Engine::latest_per_lane(const std::vector<EventRef>& deps, int skip_lane) {
+  std::vector<const EventObj*> out;
+  for (const EventRef& d : deps) {
+    if (!d || d->lane == skip_lane) continue;
+    auto it = std::find_if(out.begin(), out.end(), [&](const EventObj* e) { return e->lane == d->lane; });
+    if (it == out.end()) out.push_back(d.get());
+    else if (d->seq > (*it)->seq) *it = d.get();
+  }
+  return out;
+}
+
 EventRef Engine::acquire_event(int lane) {
   cudaEvent_t ev = nullptr;
   {
@@ -342,13 +354,16 @@ void Engine::sync_event(const EventRef& ev, const char* what) {
   if (!ev) return;
   const auto deadline = std::chrono::steady_clock::now() + watchdog_;
   auto next_poll = std::chrono::steady_clock::now() + std::chrono::milliseconds(50);
-  int spins = 0;
+  // spin (yielding) for the engine's spin budget before sleeping: a sleep
+  // overshoots by the kernel's timer slack (~50 us), which a synchronous
+  // funnel pays once per collective
+  const auto spin_until = std::chrono::steady_clock::now() + spin_;
   for (;;) {
     cudaError_t e = cudaEventQuery(ev->ev);
     if (e == cudaSuccess) return;
     if (e != cudaErrorNotReady) throw_cuda(e, what, __FILE__, __LINE__);
     device_wait_tick(deadline, next_poll, what);
-    if (++spins < 64) std::this_thread::yield();
+    if (std::chrono::steady_clock::now() < spin_until) std::this_thread::yield();
     else std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
 }
@@ -363,14 +378,14 @@ void Engine::sync_lanes() {
   }
   const auto deadline = std::chrono::steady_clock::now() + watchdog_;
   auto next_poll = std::chrono::steady_clock::now() + std::chrono::milliseconds(50);
+  const auto spin_until = std::chrono::steady_clock::now() + spin_;
   for (cudaStream_t s : lanes) {
-    int spins = 0;
     for (;;) {
       cudaError_t e = cudaStreamQuery(s);
       if (e == cudaSuccess) break;
       if (e != cudaErrorNotReady) throw_cuda(e, "cudaStreamQuery", __FILE__, __LINE__);
       device_wait_tick(deadline, next_poll, "lane work");
-      if (++spins < 64) std::this_thread::yield();
+      if (std::chrono::steady_clock::now() < spin_until) std::this_thread::yield();
       else std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   }
@@ -414,13 +429,10 @@ void Engine::run_op(Operation* op) {
     try {
       bind_device();
       stream = lane_stream(op->lane);
-      // one wait per distinct event; same-lane events are already ordered
-      std::vector<const EventObj*> waits;
-      waits.reserve(op->deps.size());
-      for (const EventRef& d : op->deps)
-        if (d->lane != op->lane) waits.push_back(d.get());
-      std::sort(waits.begin(), waits.end());
-      waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
+      // one wait per other lane -- its latest event; same-lane events are
+      // already ordered (a DepCha pull over 161 keys would otherwise wait on
+      // 161 events of the producer lane, ~0.2 us of host time each)
+      const std::vector<const EventObj*> waits = latest_per_lane(op->deps, op->lane);
       hostprof::Scope prof(hostprof::kDispatchWait);
       for (const EventObj* d : waits) CSB_CUDA(cudaStreamWaitEvent(stream, d->ev, 0));
     } catch (...) {
@@ -440,6 +452,8 @@ void Engine::run_op(Operation* op) {
       hostprof::Scope prof(hostprof::kDispatchRecord);
       if (stream) {
         done = acquire_event(op->lane);
+        std::lock_guard<std::mutex> rec(rec_mu_);
+        done->seq = ++lane_seq_[static_cast<size_t>(op->lane)];
         CSB_CUDA(cudaEventRecord(done->ev, stream));
       }
     } catch (...) {
@@ -530,11 +544,10 @@ void Engine::stream_wait(const std::vector<Tag>& tags, cudaStream_t stream) {
       for (const EventRef& r : var.readers) evs.push_back(r);
     }
   }
-  std::sort(evs.begin(), evs.end());
-  evs.erase(std::unique(evs.begin(), evs.end()), evs.end());
-  if (evs.empty()) return;
+  const std::vector<const EventObj*> waits = latest_per_lane(evs, -1);
+  if (waits.empty()) return;
   bind_device();
-  for (const EventRef& e : evs) CSB_CUDA(cudaStreamWaitEvent(stream, e->ev, 0));
+  for (const EventObj* e : waits) CSB_CUDA(cudaStreamWaitEvent(stream, e->ev, 0));
 }
 
 void Engine::wait_all() {

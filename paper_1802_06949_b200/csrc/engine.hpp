@@ -62,6 +62,10 @@ class Engine;
 struct EventObj {
   cudaEvent_t ev = nullptr;
   int lane = -1;
+  // position in its lane's record order: a wait for the latest event of a
+  // lane covers every earlier one (stream order), so dependency lists keep
+  // one event per lane
+  uint64_t seq = 0;
 };
 using EventRef = std::shared_ptr<EventObj>;
 
@@ -153,6 +157,7 @@ class Engine {
   void drain_inline();                // no lock held
   VarRecord& var_for(const Tag& tag); // mu_ held
   EventRef acquire_event(int lane);
+  static std::vector<const EventObj*> latest_per_lane(const std::vector<EventRef>& deps, int skip_lane);
   void sync_event(const EventRef& ev, const char* what);
   void sync_lanes();
   void device_wait_tick(std::chrono::steady_clock::time_point deadline,
@@ -186,6 +191,8 @@ class Engine {
 
   std::vector<cudaStream_t> lanes_;
   mutable std::mutex lanes_mu_;
+  std::mutex rec_mu_;  // seq assignment and cudaEventRecord in one step (same order)
+  std::vector<uint64_t> lane_seq_;  // per lane, sized at construction
 
   std::shared_ptr<struct EventPool> pool_;
 };

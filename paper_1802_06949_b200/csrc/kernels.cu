@@ -909,6 +909,11 @@ struct P2PParams {
   int pack;       // stage the gradients (entry d) into this rank's bucket (entry a) before barrier 0
   uint32_t epoch;
   uint64_t piece;  // groups per piece of the interleaved CTA map (0: one contiguous range per CTA)
+  // direct: phase 1 reads every rank's gradients in place -- rank r's copy of
+  // entry e is gbase[r] + (e.d - gbase[rank]) (registered regions, identical
+  // layout on every rank) -- instead of staged bucket copies; nothing is packed
+  int direct;
+  void* gbase[CS_MAX_RANKS];
 };
 
 // CTA c's share of shard s: the shard is cut into G x K equal pieces
@@ -1005,12 +1010,86 @@ __device__ __forceinline__ bool pair_barrier(const P2PParams& p, int phase) {
   return s_abort == 0;
 }
 
+// Phase 1 of the direct form: bucket groups [a, b), every rank's values read
+// in place from its registered gradients, summed in rank order exactly as the
+// staged form sums bucket copies; sink(q, acc) consumes group q's sum.
+// Groups between keys (bucket padding) are skipped; the partial last group of
+// a key reads its n % 8 elements and sums zeros beyond them, as the
+// zero-padded bucket slot would.  A thread walks its groups in increasing
+// order, so its entry only moves forward (one search per range).
+template <int CDT, int M, typename Sink>
+__device__ __forceinline__ void direct_reduce_range(const P2PParams& p, uint64_t a, uint64_t b, Sink&& sink) {
+  using Acc = typename AccOf<CDT, CDT>::T;
+  using T = typename Elem<CDT>::T;
+  constexpr int NT = reduce_threads<M>();
+  const int m = (M > 0) ? M : p.nranks;
+  if (threadIdx.x >= NT || a >= b || p.n_entries == 0) return;
+  int lo = 0, hi = p.n_entries;  // first entry with gend > a
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p.tab[mid].gend <= a) lo = mid + 1;
+    else hi = mid;
+  }
+  int e = lo;
+  const char* mine = static_cast<const char*>(p.gbase[p.rank]);
+  for (uint64_t q = a + threadIdx.x; q < b; q += NT) {
+    while (e < p.n_entries && p.tab[e].gend <= q) ++e;
+    if (e >= p.n_entries) return;
+    const uint64_t gstart = p.tab[e].gstart, n = p.tab[e].n;
+    if (q < gstart) continue;  // padding between keys
+    const uint64_t off = static_cast<uint64_t>(static_cast<const char*>(p.tab[e].d) - mine);
+    const uint64_t el = (q - gstart) * kVec;
+    Acc acc[kVec];
+    if (el + kVec <= n) {
+      if constexpr (M > 0) {
+        Acc x[M][kVec];
+#pragma unroll
+        for (int r = 0; r < M; ++r) load8_rw<CDT, Acc>(static_cast<const char*>(p.gbase[r]) + off, el, x[r]);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) acc[j] = x[0][j];
+#pragma unroll
+        for (int r = 1; r < M; ++r)
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[r][j]);
+      } else {
+        load8_rw<CDT, Acc>(static_cast<const char*>(p.gbase[0]) + off, el, acc);
+        for (int r = 1; r < m; ++r) {
+          Acc x[kVec];
+          load8_rw<CDT, Acc>(static_cast<const char*>(p.gbase[r]) + off, el, x);
+#pragma unroll
+          for (int j = 0; j < kVec; ++j) acc[j] = add_rn(acc[j], x[j]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        acc[j] = Acc(0);
+        if (el + j < n) {
+          acc[j] = to_acc<Acc>(reinterpret_cast<const T*>(static_cast<const char*>(p.gbase[0]) + off)[el + j]);
+          for (int r = 1; r < m; ++r)
+            acc[j] = add_rn(acc[j], to_acc<Acc>(reinterpret_cast<const T*>(static_cast<const char*>(p.gbase[r]) +
+                                                                              off)[el + j]));
+        }
+      }
+    }
+    sink(q, acc);
+  }
+}
+
 template <int CDT, int M>
 __device__ __forceinline__ void p2p_reduce_chunk(const P2PParams& p, uint64_t a, uint64_t b) {
   using Acc = typename AccOf<CDT, CDT>::T;
   const int m = (M > 0) ? M : p.nranks;
   constexpr int NT = reduce_threads<M>();
   if (threadIdx.x >= NT) return;
+  if (p.direct) {
+    direct_reduce_range<CDT, M>(p, a, b, [&](uint64_t q, const Acc (&acc)[kVec]) {
+      if (p.shard_only) store8<CDT, Acc>(p.bufs[p.rank], q * kVec, acc);
+      else
+        for (int r = 0; r < m; ++r) store8<CDT, Acc>(p.bufs[r], q * kVec, acc);
+    });
+    return;
+  }
   for (uint64_t q = a + threadIdx.x; q < b; q += NT) {
     const uint64_t i = q * kVec;
     Acc acc[kVec];
@@ -1162,7 +1241,7 @@ __device__ __forceinline__ void p2p_update_range(const P2PParams& p, int owner, 
 template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
   if constexpr (UPDATE && !NVLS) {
-    if (p.pack) p2p_pack_column<CDT>(p);
+    if (p.pack && !p.direct) p2p_pack_column<CDT>(p);
   }
   if (!pair_barrier(p, 0)) return;
   for_pieces(p, p.rank, [&](uint64_t, uint64_t a, uint64_t b) {
@@ -1220,8 +1299,24 @@ __device__ __forceinline__ void zero_reduce_update(const P2PParams& p, uint64_t 
   constexpr int NT = reduce_threads<M>();
   if (threadIdx.x >= NT) return;
   void* wm = p.wm[p.rank];
+  // kernel (c) on the master shard, the sum still in registers
+  auto update = [&](uint64_t q, const CAcc (&acc)[kVec]) {
+    const uint64_t j = (q - s0) * kVec;  // shard-local element
+    WAcc w[kVec], mv[kVec] = {};
+    load8_rw<WDT, WAcc>(wm, j, w);
+    if constexpr (MOM) load8_rw<MDT, WAcc>(p.mom_b, j, mv);
+#pragma unroll
+    for (int v = 0; v < kVec; ++v)
+      sgd_elem<MOM>(w[v], static_cast<WAcc>(comm_rounded<CDT>(acc[v])), mv[v], step, mu);
+    store8<WDT, WAcc>(wm, j, w);
+    if constexpr (MOM) store8<MDT, WAcc>(p.mom_b, j, mv);
+  };
+  if (p.direct) {
+    direct_reduce_range<CDT, M>(p, a, b, update);
+    return;
+  }
   for (uint64_t q = a + threadIdx.x; q < b; q += NT) {
-    const uint64_t i = q * kVec, j = (q - s0) * kVec;  // bucket element / shard-local element
+    const uint64_t i = q * kVec;  // bucket element
     CAcc acc[kVec];
     if constexpr (M > 0) {
       CAcc x[M][kVec];
@@ -1242,14 +1337,7 @@ __device__ __forceinline__ void zero_reduce_update(const P2PParams& p, uint64_t 
         for (int v = 0; v < kVec; ++v) acc[v] = add_rn(acc[v], x[v]);
       }
     }
-    WAcc w[kVec], mv[kVec] = {};
-    load8_rw<WDT, WAcc>(wm, j, w);
-    if constexpr (MOM) load8_rw<MDT, WAcc>(p.mom_b, j, mv);
-#pragma unroll
-    for (int v = 0; v < kVec; ++v)
-      sgd_elem<MOM>(w[v], static_cast<WAcc>(comm_rounded<CDT>(acc[v])), mv[v], step, mu);
-    store8<WDT, WAcc>(wm, j, w);
-    if constexpr (MOM) store8<MDT, WAcc>(p.mom_b, j, mv);
+    update(q, acc);
   }
 }
 
@@ -1281,7 +1369,7 @@ __device__ __forceinline__ void zero_gather(const P2PParams& p, int s, uint64_t 
 
 template <int CDT, int WDT, bool MOM, int M>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_constant__ P2PParams p) {
-  if (p.pack) p2p_pack_column<CDT>(p);
+  if (p.pack && !p.direct) p2p_pack_column<CDT>(p);
   if (!pair_barrier(p, 0)) return;
   for_pieces(p, p.rank, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b); });
   __syncthreads();
@@ -1969,6 +2057,12 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     if (!aligned16(a.wm[r])) throw UsageError("p2p_allreduce: master shard not 16-byte aligned");
   }
   p.mom_b = a.mom_b;
+  p.direct = (a.direct && a.update && a.tab && a.n_entries > 0 && !a.mc) ? 1 : 0;
+  if (a.direct && !p.direct) throw UsageError("p2p_allreduce: direct gradient reads need the fused update over peer memory");
+  for (int r = 0; p.direct && r < a.nranks; ++r) {
+    p.gbase[r] = a.gbase[r];
+    if (!aligned16(a.gbase[r])) throw UsageError("p2p_allreduce: gradient region not 16-byte aligned");
+  }
   p.abort_word = a.abort_word;
   static const uint64_t piece = [] {
     const char* e = std::getenv("CSB_P2P_PIECE");  // identical on every rank (same environment)

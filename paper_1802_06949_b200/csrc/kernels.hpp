@@ -105,6 +105,11 @@ struct P2PArgs {
   bool zero = false;
   void* wm[CS_MAX_RANKS] = {};
   void* mom_b = nullptr;
+  // direct: phase 1 reads every rank's gradients in place (entry d = this
+  // rank's copy; rank r's = gbase[r] + (d - gbase[rank])) -- registered
+  // regions with the same layout on every rank; nothing is staged
+  bool direct = false;
+  void* gbase[CS_MAX_RANKS] = {};
   double lr = 0, rescale = 0, momentum = 0;
   // every rank's grid on the SAME device (local peer transport): cap each
   // grid so all `nranks` grids are co-resident, plain (non-cooperative) launch

@@ -102,7 +102,10 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   // overlaps bucket b+1's collective; the engine's events order each key.
   world_lane_ = engine_.new_lane(cfg_.comm_priority);
   if (cfg_.mode == KvMode::ConCom)
-    for (int i = 0; i < cfg_.outstanding; ++i) comm_lanes_.push_back(engine_.new_lane(cfg_.comm_priority));
+    for (int i = 0; i < cfg_.outstanding; ++i) {
+      comm_lanes_.push_back(engine_.new_lane(cfg_.comm_priority));
+      comm_order_tags_.push_back(engine_.new_variable());
+    }
   pack_lane_ = engine_.new_lane(cfg_.comm_priority);
   update_lane_ = engine_.new_lane(0);
   // CSB_KV_LANES=1: packs, world collectives and updates share one stream
@@ -402,6 +405,8 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
         const int k = keys[static_cast<size_t>(i)];
         const TensorSlot& g = grads[static_cast<size_t>(i)];
         if (g.data == key_ptr(k) && g.dtype == comm_dt_) continue;  // a bucket view
+        if (defer_src_.size() != keys_.size()) defer_src_.assign(keys_.size(), nullptr);
+        defer_src_[static_cast<size_t>(k)] = entries[j].src;
         B.deferred.push_back({k, entries[j++]});
       }
       B.deferred_reads.insert(B.deferred_reads.end(), reads.begin(), reads.end());
@@ -432,14 +437,19 @@ void KvStore::push_pack_op(Bucket& B, const std::vector<cs_copy_entry>& entries,
       reads, {B.tag}, OpKind::Copy, key0, pack_lane_, Dispatch::Inline);
 }
 
+void KvStore::clear_deferred(Bucket& B) {
+  for (const auto& [k, e] : B.deferred) defer_src_[static_cast<size_t>(k)] = nullptr;
+  B.deferred.clear();
+  B.deferred_reads.clear();
+  B.deferred_dt = -1;
+}
+
 void KvStore::flush_deferred(Bucket& B) {
   if (B.deferred.empty() && B.deferred_reads.empty()) return;
   std::vector<cs_copy_entry> entries;
   for (const auto& [k, e] : B.deferred) entries.push_back(e);
   push_pack_op(B, entries, B.deferred_reads, B.deferred_dt, B.deferred.empty() ? B.keys[0] : B.deferred[0].first);
-  B.deferred.clear();
-  B.deferred_reads.clear();
-  B.deferred_dt = -1;
+  clear_deferred(B);
 }
 
 void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
@@ -468,7 +478,16 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
     }();
     if (!async) engine_.wait_for(B.tag);
   } else {
-    // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136)
+    // offloaded collective on comms[b % outstanding] (kvstore.cpp:117-136).
+    // Collectives of one communicator are chained in push order through the
+    // communicator's order tag: two pool threads of one rank must not reach
+    // the ledger out of order, or it would pair one key's buffer with
+    // another's on the peers (equal counts match).  The reference leaves that
+    // to the caller's barrier window (one call in flight per comm);
+    // here a pushed-ahead window stays correct, and the communicators still
+    // run concurrently with each other.
+    for (size_t i = 0; i < comm_lanes_.size(); ++i)
+      if (comm_lanes_[i] == B.lane) muts.push_back(comm_order_tags_[i]);
     std::atomic<int>* outstanding = &outstanding_;
     outstanding_.fetch_add(1);
     std::vector<Tag> reads;
@@ -629,8 +648,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
           es.push_back(DeviceTable::Entry{updates[j].g, updates[j].mom, updates[j].w, updates[j].n, g0,
                                           g0 + (updates[j].n + 7) / 8});
           if (fuse_p2p)  // the kernel stages this key's gradient (d) into its slot (a)
-            for (const auto& [dk, e] : B.deferred)
-              if (dk == k) es.back().d = const_cast<void*>(e.src);
+            if (const void* src = deferred_src(k)) es.back().d = const_cast<void*>(src);
         }
         std::vector<Tag> p2p_reads;
         if (fuse_p2p) {
@@ -638,17 +656,36 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
           for (const Tag& t : B.deferred_reads)
             if (std::none_of(B.view_tags.begin(), B.view_tags.end(), [&](const Tag& v) { return v.id == t.id; }))
               p2p_reads.push_back(t);
-          B.deferred.clear();
-          B.deferred_reads.clear();
-          B.deferred_dt = -1;
+          clear_deferred(B);
         }
         std::sort(es.begin(), es.end(), [](const auto& x, const auto& y) { return x.gstart < y.gstart; });
+        // direct: every staged gradient lies in the registered region -> the
+        // kernel reads all ranks' copies in place and stages nothing.  The
+        // (slot, offset) layout is hashed into the ledger signature, so ranks
+        // whose regions are laid out differently fail with MismatchError
+        // before any launch instead of reading wrong addresses.
+        bool direct = fuse_p2p && !greg_peers_.empty();
+        uint64_t layout = 1469598103934665603ull;  // FNV-1a
+        for (const auto& e : es) {
+          if (!direct) break;
+          const char* d = static_cast<const char*>(e.d);
+          const char* base = static_cast<const char*>(greg_base_);
+          if (!d || d == e.a || d < base || d + e.n * dtype_size(comm_dt_) > base + greg_bytes_ ||
+              (reinterpret_cast<uintptr_t>(d) & 15u) != 0) {
+            direct = false;
+            break;
+          }
+          for (uint64_t v : {e.gstart, static_cast<uint64_t>(d - base)}) {
+            layout ^= v;
+            layout *= 1099511628211ull;
+          }
+        }
         if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
         DeviceTable* ptab = B.p2p_tab.get();  // all its uploads on B.lane
         for (const Tag& t : out_tags) muts.push_back(t);
         const bool zero = zero_active_;
         engine_.push_stream(
-            [self, bi, es, ptab, out_dt, opt, whole, zero, fuse_p2p](cudaStream_t s) {
+            [self, bi, es, ptab, out_dt, opt, whole, zero, fuse_p2p, direct, layout](cudaStream_t s) {
               Bucket& Bk = self->buckets_[bi];
               Transport::P2PUpdate u;
               u.tab = ptab->resident(es, s);
@@ -658,7 +695,11 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
               u.rescale = opt.rescale;
               u.momentum = opt.momentum;
               u.shard_only = whole;
-              u.pack = fuse_p2p;
+              u.pack = fuse_p2p && !direct;
+              if (direct) {
+                u.gbase = self->greg_peers_.data();
+                u.layout = layout;
+              }
               if (zero) {
                 if (!Bk.master_ready) self->zero_fill_master(Bk, es, out_dt, s);
                 u.wm = Bk.wm_peers.data();
@@ -688,8 +729,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
         const int k = keys[static_cast<size_t>(i)];
         const TensorSlot& o = outs[static_cast<size_t>(i)];
         const void* g = key_ptr(k);  // a bucket view: already in place
-        for (const auto& [dk, e] : B.deferred)
-          if (dk == k) g = e.src;
+        if (const void* src = deferred_src(k)) g = src;
         pu.push_back(DeviceTable::PackUpdate{g, key_ptr(k), o.data, keys_[static_cast<size_t>(k)].mom, o.numel});
       }
       std::vector<Tag> reads;
@@ -707,9 +747,7 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
             ftab->pack_sgd(pu, gdt, cdt, out_dt, opt.lr, opt.rescale, opt.momentum, s);
           },
           reads, fmuts, OpKind::Compute, key0, update_lane_, Dispatch::Inline);
-      B.deferred.clear();
-      B.deferred_reads.clear();
-      B.deferred_dt = -1;
+      clear_deferred(B);
     } else {
       engine_.push_stream(finish, buf_tags, out_tags, upd ? OpKind::Compute : OpKind::Copy, key0,
                           update_lane_, Dispatch::Inline);
@@ -723,6 +761,24 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
       B.view_tags.clear();
     }
   }
+}
+
+// Setup collective (every rank, same order): the region holding this rank's
+// gradients, mapped into every peer.  Whole-bucket pull_updates whose pushed
+// gradients all lie inside it then let the fused peer kernel read every
+// rank's gradients in place: push stages nothing (kvstore.cpp:109's copy is
+// skipped; the gradients' tags are read by the collective op, so they stay
+// unmodified until every rank has read them).
+void KvStore::register_grads(void* base, uint64_t bytes) {
+  if (!base || bytes == 0) throw UsageError("KvStore: empty gradient region");
+  if (!p2p_active_) return;  // one rank, or NCCL: staging is the only form
+  if (!greg_peers_.empty()) throw UsageError("KvStore: a gradient region is already registered");
+  engine_.bind_device();
+  std::vector<void*> peers = transport_.share_buffer(base, rank_);
+  shared_.push_back(peers);
+  greg_base_ = base;
+  greg_bytes_ = bytes;
+  greg_peers_.assign(peers.begin(), peers.end());
 }
 
 // kvstore.cpp:185-193: drain the in-flight counter, then a world barrier.

@@ -111,6 +111,10 @@ class KvStore {
   // there and pushed with that address is not copied (push only orders it);
   // the collective then rewrites it in place.  Builds the buckets.
   void* bucket_view(int key);
+  // Setup collective: register the allocation holding this rank's gradients
+  // (a cudaMalloc base, same layout on every rank) so the fused peer kernel
+  // reads them in place instead of staging them into the buckets.
+  void register_grads(void* base, uint64_t bytes);
   // The fusion-bucket arena (one allocation holding every bucket).
   void arena(void** base, uint64_t* bytes);
 
@@ -176,6 +180,17 @@ class KvStore {
   void push_pack_op(Bucket& B, const std::vector<cs_copy_entry>& entries, const std::vector<Tag>& reads, int src_dt,
                     int key0);
   void flush_deferred(Bucket& B);
+  void clear_deferred(Bucket& B);
+  // key -> staging source of its deferred pack (nullptr: none), kept in step
+  // with every bucket's `deferred` list: O(1) lookups in pull
+  std::vector<const void*> defer_src_;
+  // register_grads(): this rank's region and every rank's mapping of theirs
+  void* greg_base_ = nullptr;
+  uint64_t greg_bytes_ = 0;
+  std::vector<const void*> greg_peers_;
+  const void* deferred_src(int k) const {
+    return static_cast<size_t>(k) < defer_src_.size() ? defer_src_[static_cast<size_t>(k)] : nullptr;
+  }
 
   Engine& engine_;
   Transport& transport_;
@@ -190,6 +205,7 @@ class KvStore {
   int pack_lane_ = 0;
   int update_lane_ = 0;
   std::vector<int> comm_lanes_;  // concom: lane per extra communicator
+  std::vector<Tag> comm_order_tags_;  // concom: per-communicator issue-order chain
   Tag init_order_tag_;
   Tag dummy_tag_;
   Tag funnel_tag_;

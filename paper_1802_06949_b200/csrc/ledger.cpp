@@ -22,7 +22,7 @@ namespace {
 constexpr uint64_t kFree = ~0ull;
 constexpr int kInflightPerRank = 32;
 constexpr int kMsgLen = 512;
-constexpr int kDescLen = 48;
+constexpr int kDescLen = 96;  // room for the p2p variant and the direct layout hash
 constexpr int kBlobLen = 256;
 }  // namespace
 
@@ -46,6 +46,7 @@ std::string describe_call(const CallSig& sig) {
       if (sig.variant & kVarUpdate) os << "+update";
       if (sig.variant & kVarShardOnly) os << "+shard_only";
       if (sig.variant & kVarZero) os << "+zero";
+      if (sig.variant & kVarDirect) os << "+direct(layout " << std::hex << sig.layout << std::dec << ")";
     }
     os << ")";
   } else if (sig.kind == CollKind::Broadcast) {

@@ -41,8 +41,13 @@ struct CallSig {
   // B200 extension: peer-memory kernels pair CTAs across ranks, so every rank
   // must launch the same barrier protocol (CallVariant bits); 0 = plain call
   int32_t variant = 0;
+  // kVarDirect: hash of the gradients' (key, offset in the registered region)
+  // layout, which must be identical on every rank (peers address each other's
+  // gradients by this rank's offsets)
+  uint64_t layout = 0;
   bool operator==(const CallSig& o) const {
-    return kind == o.kind && count == o.count && root == o.root && dtype == o.dtype && variant == o.variant;
+    return kind == o.kind && count == o.count && root == o.root && dtype == o.dtype && variant == o.variant &&
+           layout == o.layout;
   }
 };
 
@@ -53,6 +58,7 @@ enum CallVariant : int32_t {
   kVarShardOnly = 4,  // update reads the owners' shards; trailing barrier
   kVarZero = 8,       // ZeRO-1 form
   kVarNvls = 16,      // NVSwitch multicast reduction
+  kVarDirect = 32,    // phase 1 reads every rank's gradients in place (registered region, no staging)
 };
 
 std::string describe_call(const CallSig& sig);

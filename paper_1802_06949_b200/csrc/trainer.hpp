@@ -38,6 +38,7 @@ struct SynthConfig {
   int p2p = 0;               // NVLink peer-memory collectives (KvConfig::p2p)
   bool grad_views = false;   // produce gradients in place in the comm buckets (KvStore::bucket_view)
   int zero = 0;              // ZeRO-1 sharded update (KvConfig::zero)
+  bool direct_grads = false; // register the gradient arena (KvStore::register_grads): in-place peer reads
   int order_seed = 0;        // != 0: per-rank random gradient-ready order (deadlock stress)
   uint64_t seed_base = 1000;
   // Measured gradient-ready time of every key from the start of a real

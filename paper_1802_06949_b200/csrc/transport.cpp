@@ -1,6 +1,8 @@
 // transport.cpp -- see transport.hpp.
 #include "transport.hpp"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -215,22 +217,43 @@ std::vector<void*> Transport::share_buffer(void* base, int rank) {
   if (share_slots_ >= kLedgerRankBlobSlots - 1) throw ConfigError("Transport: too many shared buffers");
   const int slot = share_slots_++;
   CSB_CUDA(cudaSetDevice(device_));
-  cudaIpcMemHandle_t h;
-  CSB_CUDA(cudaIpcGetMemHandle(&h, base));
-  static_assert(sizeof(cudaIpcMemHandle_t) <= kRankBlobLen, "IPC handle does not fit the mailbox");
-  ledger_->post_rank_blob(slot, rank_, &h, sizeof(h));
+  // an IPC handle names the whole allocation (a peer's mapping starts at its
+  // base), so `base` may be an interior pointer: post the handle together
+  // with base's offset inside its allocation
+  struct Blob {
+    cudaIpcMemHandle_t h;
+    uint64_t offset;
+  } blob{};
+  static_assert(sizeof(Blob) <= kRankBlobLen, "IPC handle does not fit the mailbox");
+  CSB_CUDA(cudaIpcGetMemHandle(&blob.h, base));
+  {
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+      void* fp = nullptr;
+      cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+      CSB_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q));
+      if (!fp || q != cudaDriverEntryPointSuccess) throw CudaError("driver entry point missing: cuMemGetAddressRange");
+      return reinterpret_cast<GetRange>(fp);
+    }();
+    CUdeviceptr alloc = 0;
+    size_t alloc_bytes = 0;
+    if (get_range(&alloc, &alloc_bytes, reinterpret_cast<CUdeviceptr>(base)) != CUDA_SUCCESS)
+      throw UsageError("Transport: share_buffer of memory that is not a device allocation");
+    blob.offset = reinterpret_cast<CUdeviceptr>(base) - alloc;
+  }
+  ledger_->post_rank_blob(slot, rank_, &blob, sizeof(blob));
   std::vector<void*> ptrs(static_cast<size_t>(num_ranks()), nullptr);
   for (int r = 0; r < num_ranks(); ++r) {
     if (r == rank_) {
       ptrs[r] = base;
       continue;
     }
-    cudaIpcMemHandle_t ph;
-    ledger_->read_rank_blob(slot, r, &ph, sizeof(ph));
+    Blob pb{};
+    ledger_->read_rank_blob(slot, r, &pb, sizeof(pb));
     void* p = nullptr;
-    CSB_CUDA(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
-    ipc_opened_.push_back(p);
-    ptrs[r] = p;
+    CSB_CUDA(cudaIpcOpenMemHandle(&p, pb.h, cudaIpcMemLazyEnablePeerAccess));
+    ptrs[r] = static_cast<char*>(p) + pb.offset;
+    ipc_opened_.push_back({p, ptrs[r]});
   }
   return ptrs;
 }
@@ -241,9 +264,10 @@ void Transport::unshare_buffer(const std::vector<void*>& ptrs) {
   cudaSetDevice(device_);
   for (size_t r = 0; r < ptrs.size(); ++r) {
     if (static_cast<int>(r) == rank_ || !ptrs[r]) continue;
-    auto it = std::find(ipc_opened_.begin(), ipc_opened_.end(), ptrs[r]);
+    auto it = std::find_if(ipc_opened_.begin(), ipc_opened_.end(),
+                           [&](const std::pair<void*, void*>& o) { return o.second == ptrs[r]; });
     if (it == ipc_opened_.end()) continue;
-    cudaIpcCloseMemHandle(*it);
+    cudaIpcCloseMemHandle(it->first);
     ipc_opened_.erase(it);
   }
 }
@@ -338,7 +362,9 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   // every rank must run the same barrier protocol (a shard_only
   // rank would wait at a phase-2 barrier its peers never reach)
   sig.variant = kVarP2P | (mc ? kVarNvls : 0) | (upd ? kVarUpdate : 0) |
-                (upd && upd->shard_only && !mc ? kVarShardOnly : 0) | (upd && upd->wm ? kVarZero : 0);
+                (upd && upd->shard_only && !mc ? kVarShardOnly : 0) | (upd && upd->wm ? kVarZero : 0) |
+                (upd && upd->gbase && !mc ? kVarDirect : 0);
+  if (sig.variant & kVarDirect) sig.layout = upd->layout;
   Ledger::Ticket t;
   {
     hostprof::Scope prof(hostprof::kLedger);
@@ -372,6 +398,10 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
     a.momentum = upd->momentum;
     a.shard_only = upd->shard_only && !mc;
     a.pack = upd->pack && !mc;
+    if (upd->gbase && !mc) {
+      a.direct = true;
+      for (int r = 0; r < num_ranks(); ++r) a.gbase[r] = const_cast<void*>(upd->gbase[r]);
+    }
     if (upd->wm) {
       a.zero = true;
       for (int r = 0; r < num_ranks(); ++r) a.wm[r] = const_cast<void*>(upd->wm[r]);
@@ -430,7 +460,7 @@ Transport::~Transport() {
   if (backend_ == Backend::Nccl) {
     const bool aborted = ledger_ && ledger_->latched();
     cudaSetDevice(device_);
-    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (const auto& o : ipc_opened_) cudaIpcCloseMemHandle(o.first);
     for (void* p : own_flags_) cudaFree(p);
     for (ncclComm_t c : comms_) {
       if (!c) continue;

@@ -103,6 +103,11 @@ class Transport {
     bool pack = false;        // entries' d = gradients: the kernel stages them first (kernel (a) folded in)
     const void* const* wm = nullptr;  // ZeRO-1: every rank's master shard; null = replicated update
     void* mom_b = nullptr;            // ZeRO-1: this rank's momentum shard
+    // direct gradient reads: every rank's registered gradient region (entries'
+    // d = this rank's gradients inside it); `layout` hashes the (key, offset)
+    // list, matched across ranks like the rest of the signature
+    const void* const* gbase = nullptr;
+    uint64_t layout = 0;
   };
   // Allreduce of one bucket through peer memory, matched by the ledger like
   // allreduce_sum; with `upd`, fused with the SGD / momentum update of the
@@ -153,7 +158,7 @@ class Transport {
   bool nvls_ok_ = false;
   std::string name_;
   int share_slots_ = 0;
-  std::vector<void*> ipc_opened_;
+  std::vector<std::pair<void*, void*>> ipc_opened_;  // (opened allocation base, pointer handed out)
   std::vector<void*> own_flags_;
   std::vector<std::vector<void*>> flags_;  // comm -> every rank's flag region
 };

@@ -16,7 +16,9 @@ the producer is PyTorch autograd on its own CUDA stream:
   the bucket (shard_only; the rest still holds this rank's own gradient), and
   with ``zero=True`` no sum at all (the reduction stays in registers).  Code
   that reads p.grad after step() (clipping, logging) must read it before
-  step() or run with ``p2p=0``;
+  step() or run with ``p2p=0``.  At world > 1 over the peer-memory kernel the
+  arena is registered (``direct_grads``, KvStore.register_grads): the fused
+  kernel reads every rank's gradients in place, so push stages nothing;
 * a post-accumulate-grad hook counts ready gradients per fusion bucket; when a
   bucket is complete it records a CUDA event on the autograd stream,
   ``Engine.import_event`` turns it into the latest write of the gradients
@@ -55,7 +57,7 @@ class TorchKvStoreDP:
                  world: int, *, mode: str = "depcha", lr: float = 0.1, momentum: float = 0.0,
                  rescale: float | None = None, bucket_mb: float = 25.0, p2p: int = 1, outstanding: int = 1,
                  concom_comms: Sequence[int] = (), comm_dtype: int = -1, bucket_views: bool = False,
-                 zero: bool = False):
+                 zero: bool = False, direct_grads: bool = True):
         if mode not in ("depcha", "funnel"):
             raise ValueError("TorchKvStoreDP drives the DepCha / Funnel schedules (push during backward, "
                              "pull after it)")
@@ -96,6 +98,10 @@ class TorchKvStoreDP:
         torch.cuda.synchronize(dev)  # the weights were written on the framework stream
         for k in range(K):
             self.kv.init(k, self.w_slots[k])  # rank 0's weights broadcast (kvstore.cpp:95)
+        if direct_grads and not bucket_views and world > 1 and p2p == 1:
+            # the flat arena is registered (a setup collective): the fused peer
+            # kernel reads every rank's gradients in place, nothing is staged
+            self.kv.register_grads(self.grad_arena.data_ptr(), self.grad_arena.numel() * esz)
         # gradient-ready groups = fusion buckets (built here, identically on every rank)
         groups: dict[int, list[int]] = {}
         for k in range(K):

@@ -184,6 +184,55 @@ def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False):
                 store.close()
                 eng.close()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)
+    elif case in ("direct", "direct_mismatch"):
+        # gradients in one registered region (KvStore.register_grads): the
+        # fused peer kernels read every rank's gradients in place instead of
+        # staging them; weights must equal the staged run's bit for bit.
+        # direct_mismatch: each rank lays its keys out at rank-dependent
+        # offsets -> MismatchError before any launch (layout in the signature)
+        sizes = [1, 7, 64, 300, 4097, 70000, 1 << 18]
+        K = len(sizes)
+        res = {}
+        variants = ([(z, g, d) for z in (0, 1) for g in (api.F32, api.BF16) for d in (0, 1)]
+                    if case == "direct" else [(1, api.F32, 1)])
+        for zero, gdt, direct in variants:
+            tdt, esz = (torch.float32, 4) if gdt == api.F32 else (torch.bfloat16, 2)
+            shift = 256 * rank if case == "direct_mismatch" else 0
+            offs, o = [], shift
+            for n in sizes:
+                offs.append(o)
+                o += (n * esz + 255) // 256 * 256
+            garena = torch.zeros(o, dtype=torch.uint8, device=dev)
+            eng = Engine(4, rank, None, local)
+            store = KvStore(eng, tr, rank, KvConfig("depcha", 1, K, comm_dtype=gdt, bucket_bytes=256 * 1024,
+                                                    issue_order=1, p2p=1, zero=zero))
+            ws = [Slot(torch.from_numpy(np.ascontiguousarray(
+                O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n), dtype=np.float32)).to(dev),
+                eng.new_variable()) for k, n in enumerate(sizes)]
+            gs = []
+            for k, n in enumerate(sizes):
+                g = garena[offs[k]:offs[k] + n * esz].view(tdt)
+                g.copy_(torch.from_numpy(O.random_uniform(n, 1000 + rank * K + k)).to(dev).to(tdt))
+                gs.append(Slot(g, eng.new_variable()))
+            for k in range(K):
+                store.init(k, ws[k])
+            eng.wait_all()
+            if direct:
+                store.register_grads(garena.data_ptr(), garena.numel())
+            try:
+                for _ in range(3):
+                    store.push(list(range(K)), gs)
+                    store.pull_update(list(range(K)), ws, 0.1, 1.0 / 64, 0.9)
+                eng.wait_all()
+                out["error"] = None
+            except MismatchError as e:
+                out["error"] = type(e).__name__ + ": " + str(e)
+            if out.get("error") is None:
+                for k in range(K):
+                    res[f"z{zero}_g{gdt}_d{direct}_k{k}"] = ws[k].value.cpu().numpy()
+            store.close()
+            eng.close()
+        np.savez(outdir / f"{case}_r{rank}.npz", **res)
     elif case in ("torch_dp", "torch_dp_zero"):
         # real-backward producer over the fused NVLink kernel: save every
         # rank's per-step gradients and weights; the test replays the oracle

@@ -124,3 +124,34 @@ def check_zero_vs_oracle(d: Path, R: int):
         for _ in range(3):
             w, m = O.sgd_update(w, g, 0.1, 1.0 / 64, 0.9, m, kind="f32")
         np.testing.assert_array_equal(o[f"z1_c1_k{k}"], w, err_msg=f"R={R} key {k}")
+
+
+def check_direct(d: Path, R: int):
+    """Direct gradient reads (registered region, nothing staged) give the
+    staged run's weights bit for bit -- ZeRO-1 and replicated, fp32 and bf16
+    gradients -- on every rank, and the fp32 ZeRO-1 run equals the f32 oracle."""
+    outs = [np.load(d / f"direct_r{r}.npz") for r in range(R)]
+    for r in range(R):
+        names = [n for n in outs[r].files if "_d1_" in n]
+        assert len(names) == 4 * 7, names
+        for name in names:
+            np.testing.assert_array_equal(outs[r][name], outs[r][name.replace("_d1_", "_d0_")],
+                                          err_msg=f"R={R} rank {r} {name}")
+            np.testing.assert_array_equal(outs[r][name], outs[0][name])
+    sizes = [1, 7, 64, 300, 4097, 70000, 1 << 18]
+    K = len(sizes)
+    for k, n in enumerate(sizes):
+        w = O.random_uniform(n, O.mix_seed(7, k)).astype(np.float32)
+        g = O.rank_order_sum([O.random_uniform(n, 1000 + r * K + k).astype(np.float32) for r in range(R)], "f32")
+        m = np.zeros(n, np.float32)
+        for _ in range(3):
+            w, m = O.sgd_update(w, g, 0.1, 1.0 / 64, 0.9, m, kind="f32")
+        np.testing.assert_array_equal(outs[0][f"z1_g1_d1_k{k}"], w, err_msg=f"R={R} key {k}")
+
+
+def check_direct_mismatch(outs, R: int):
+    """Rank-dependent gradient layouts are caught by the ledger (layout hash
+    in the call signature) before any peer kernel reads a wrong address."""
+    for r in range(R):
+        assert outs[r]["error"] and outs[r]["error"].startswith("MismatchError"), outs[r]
+        assert "direct" in outs[r]["error"], outs[r]["error"]

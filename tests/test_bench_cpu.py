@@ -56,4 +56,5 @@ def test_reference_arm_runs_n_rank_threads_without_the_package():
 
     class A:
         config, issue_order, momentum, grad_views = "uniform16", "descending", 0.9, False
+        direct, comm = True, None
     assert line["config"] == bench.config_dict(A, keys, mode, outstanding, dtype, bucket_mb, 2)

@@ -15,8 +15,8 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from peer_cases import (check_p2p_api, check_schedule_weights, check_stress_order, check_torch_dp,
-                        check_zero_vs_oracle, check_zero_vs_replicated)
+from peer_cases import (check_direct, check_direct_mismatch, check_p2p_api, check_schedule_weights,
+                        check_stress_order, check_torch_dp, check_zero_vs_oracle, check_zero_vs_replicated)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 HERE = Path(__file__).resolve().parent
@@ -133,6 +133,18 @@ def test_zero_equals_replicated_update_fp32_and_bf16(two_gpus, tmp_path):
         run_case("zero_vs_replicated", R, d)
         check_zero_vs_replicated(d, R)
         check_zero_vs_oracle(d, R)
+
+
+def test_direct_gradient_reads_over_ipc_equal_staged(two_gpus, tmp_path):
+    """register_grads over CUDA IPC (an interior pointer of a torch
+    allocation: the handle names the allocation, the offset travels with
+    it): in-place peer reads of every rank's gradients == the staged run."""
+    for R in world_sizes(two_gpus):
+        d = tmp_path / f"R{R}"
+        d.mkdir()
+        run_case("direct", R, d)
+        check_direct(d, R)
+    check_direct_mismatch(run_case("direct_mismatch", 2, tmp_path), 2)
 
 
 def test_nvls_fused_allreduce_update_within_tolerance(two_gpus, tmp_path):

@@ -19,8 +19,8 @@ import pytest
 import torch
 
 from mp_worker import run_colocated
-from peer_cases import (check_p2p_api, check_schedule_weights, check_stress_order, check_torch_dp,
-                        check_zero_vs_oracle, check_zero_vs_replicated)
+from peer_cases import (check_direct, check_direct_mismatch, check_p2p_api, check_schedule_weights,
+                        check_stress_order, check_torch_dp, check_zero_vs_oracle, check_zero_vs_replicated)
 
 pytestmark = pytest.mark.gpu
 RANKS = [2, 4, 8]
@@ -48,7 +48,17 @@ def test_colocated_zero_equals_replicated_and_oracle(gpu, tmp_path, R):
     check_zero_vs_oracle(tmp_path, R)
 
 
-@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("R", RANKS)
+def test_colocated_direct_gradient_reads_equal_staged(gpu, tmp_path, R):
+    run_colocated("direct", R, tmp_path)
+    check_direct(tmp_path, R)
+
+
+def test_colocated_direct_layout_mismatch_raises(gpu, tmp_path):
+    check_direct_mismatch(run_colocated("direct_mismatch", 2, tmp_path, watchdog_ms=5000), 2)
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
 def test_colocated_stress_random_completion_order(gpu, tmp_path, R):
     check_stress_order(R, run_colocated("stress_order", R, tmp_path))
 
