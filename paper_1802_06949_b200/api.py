@@ -30,11 +30,27 @@ import json
 import os
 import tempfile
 import threading
+import weakref
 from dataclasses import dataclass
 from typing import Callable, Iterable, Sequence
 
 from . import _lib
 from ._lib import check, lib
+
+
+def _close_children(parent) -> None:
+    """An Engine / Transport outlives every KvStore / SynthModel built on it:
+    closing the parent first closes its live children, so no native
+    destructor (a KvStore drains its engine) ever runs against an engine or a
+    transport that is already gone -- whichever order the caller, or the
+    garbage collector on some other thread, gets to them."""
+    for child in list(getattr(parent, "_children", ())):
+        child.close()
+
+
+def _adopt(child, *parents) -> None:
+    for p in parents:
+        p._children.add(child)
 
 try:  # torch is plumbing: device memory and streams
     import torch
@@ -131,6 +147,7 @@ class Engine:
         check(lib.cs_engine_create(num_worker_threads, rank, device, trace.h if trace else None,
                                    C.byref(h)))
         self.h = h
+        self._children = weakref.WeakSet()
         self.device = device
         self._keep: dict[int, object] = {}
         self._keep_mu = threading.Lock()
@@ -254,6 +271,7 @@ class Engine:
 
     def close(self):
         if self.h:
+            _close_children(self)
             lib.cs_engine_destroy(self.h)
             self.h = None
 
@@ -280,6 +298,7 @@ class Transport:
 
     def __init__(self, handle):
         self.h = handle
+        self._children = weakref.WeakSet()
 
     @staticmethod
     def world() -> int:
@@ -402,6 +421,7 @@ class Transport:
 
     def close(self):
         if self.h:
+            _close_children(self)
             lib.cs_transport_destroy(self.h)
             self.h = None
 
@@ -480,6 +500,7 @@ class KvStore:
         self.engine = engine
         self.transport = transport
         self.config = config
+        _adopt(self, engine, transport)
         self.rank = rank
 
     @staticmethod
@@ -627,6 +648,7 @@ class SynthModel:
         self.h = h
         self.engine = engine
         self.transport = transport
+        _adopt(self, engine, transport)
         self.sizes = list(sizes)
         self.w_dtype = w_dtype
 

@@ -874,13 +874,13 @@ __device__ __forceinline__ void pack_sgd_walk(const TabView& t, uint64_t total, 
 // griddepcontrol.wait until this grid has completed and flushed -- the launch
 // latency between two steps overlaps the previous step's tail.  Without the
 // launch attribute both instructions are no-ops.
-template <int GDT, int CDT, int WDT, bool MOM>
+template <int GDT, int CDT, int WDT, bool MOM, int U>
 __global__ void __launch_bounds__(kThreads)
     pack_sgd_tab_kernel(const DevEntry* __restrict__ tab, const uint32_t* __restrict__ first,
                         const uint8_t* __restrict__ vec, uint64_t total, double step, double mu) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  pack_sgd_walk<GDT, CDT, WDT, MOM, kSgdU>(TabView{tab, first, vec}, total, step, mu);
+  pack_sgd_walk<GDT, CDT, WDT, MOM, U>(TabView{tab, first, vec}, total, step, mu);
 }
 
 // ------------------------- fused NVLink allreduce (+ SGD) over peer memory
@@ -1565,11 +1565,20 @@ int stream_ctas_per_sm() {
 
 template <typename Kernel>
 int wave_grid(Kernel kernel, uint64_t groups, int u = 1) {
-  static const int occ = [&] {
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess) b = 1;
-    return std::max(1, std::min(b, stream_ctas_per_sm()));
-  }();
+  // resident CTAs per SM, per kernel (instantiations share Kernel's type)
+  static std::mutex mu;
+  static std::map<const void*, int> occs;
+  int occ;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = occs.find(reinterpret_cast<const void*>(kernel));
+    if (it == occs.end()) {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess) b = 1;
+      it = occs.emplace(reinterpret_cast<const void*>(kernel), std::max(1, std::min(b, stream_ctas_per_sm()))).first;
+    }
+    occ = it->second;
+  }
   const uint64_t full = static_cast<uint64_t>(sm_count_for_current_device()) * occ;
   const uint64_t chunk = static_cast<uint64_t>(kThreads) * static_cast<uint64_t>(u);
   const uint64_t need = (groups + chunk - 1) / chunk;  // chunks: no CTA without one
@@ -2009,12 +2018,17 @@ void DeviceTable::pack_sgd(const std::vector<PackUpdate>& es, int gdt, int cdt, 
   if (host_.empty()) return;
   const double step = lr * rescale;  // model.cpp:21, fp64 on the host
   LaunchScope ls(kKernPackSgd, bytes, s);
-#define CSB_PACK_SGD(G, C, W, M)                                                              \
-  if (gdt == G && cdt == C && wdt == W && mom == M) {                                         \
-    grid_ = wave_grid(pack_sgd_tab_kernel<G, C, W, M>, groups_, kSgdU);                       \
-    sync(static_cast<uint64_t>(kThreads) * kSgdU, s);                                         \
+  // groups per thread per chunk (CSB_SGD_U = 1 or 2)
+  static const int u = [] {
+    const char* e = std::getenv("CSB_SGD_U");
+    return (e && std::atoi(e) == 2) ? 2 : 1;
+  }();
+#define CSB_PACK_SGD_U(G, C, W, M, U)                                                         \
+  if (gdt == G && cdt == C && wdt == W && mom == M && u == U) {                               \
+    grid_ = wave_grid(pack_sgd_tab_kernel<G, C, W, M, U>, groups_, U);                        \
+    sync(static_cast<uint64_t>(kThreads) * U, s);                                             \
     const char* base = static_cast<const char*>(dev_);                                        \
-    launch_pdl(pack_sgd_tab_kernel<G, C, W, M>, grid_, s, reinterpret_cast<const Entry*>(base),  \
+    launch_pdl(pack_sgd_tab_kernel<G, C, W, M, U>, grid_, s, reinterpret_cast<const Entry*>(base),  \
                reinterpret_cast<const uint32_t*>(base + host_.size() * sizeof(Entry)),         \
                reinterpret_cast<const uint8_t*>(base + host_.size() * sizeof(Entry) + first_.size() * 4), \
                groups_, step, momentum);                                                       \
@@ -2022,6 +2036,7 @@ void DeviceTable::pack_sgd(const std::vector<PackUpdate>& es, int gdt, int cdt, 
     ls.done();                                                                                \
     return;                                                                                   \
   }
+#define CSB_PACK_SGD(G, C, W, M) CSB_PACK_SGD_U(G, C, W, M, 1) CSB_PACK_SGD_U(G, C, W, M, 2)
   CSB_PACK_SGD(CS_F32, CS_F32, CS_F32, false)
   CSB_PACK_SGD(CS_F32, CS_F32, CS_F32, true)
   CSB_PACK_SGD(CS_BF16, CS_BF16, CS_F32, false)
@@ -2033,6 +2048,7 @@ void DeviceTable::pack_sgd(const std::vector<PackUpdate>& es, int gdt, int cdt, 
   CSB_PACK_SGD(CS_F64, CS_F64, CS_F64, false)
   CSB_PACK_SGD(CS_F64, CS_F64, CS_F64, true)
 #undef CSB_PACK_SGD
+#undef CSB_PACK_SGD_U
 }
 
 const DeviceTable::Entry* DeviceTable::resident(const std::vector<Entry>& es, cudaStream_t s) {

@@ -36,6 +36,19 @@ def test_colocated_fused_kernel_matches_reference_weights(gpu, tmp_path, R, mode
 
 
 @pytest.mark.parametrize("R", RANKS)
+@pytest.mark.parametrize("mode", ["funnel", "depcha", "concom"])
+def test_colocated_three_schedules_match_reference_weights(gpu, tmp_path, R, mode):
+    """The paper's three schedules with R rank threads (R = 8: the north
+    star's 8-rank case) over the in-process transport -- kernel (b)'s
+    rank-order sum as the collective, ConCom on 2 extra communicators --
+    deadlock-free, every rank's weights equal to the unmodified reference
+    KvStore's (golden, trainer.cpp:112-141 loop), identical per-comm issue
+    sequences on every rank."""
+    outs = run_colocated(mode, R, tmp_path)
+    check_schedule_weights(tmp_path, mode, mode, R, outs)
+
+
+@pytest.mark.parametrize("R", RANKS)
 def test_colocated_c_abi_reduce_and_shard_only(gpu, tmp_path, R):
     run_colocated("p2p_api", R, tmp_path)
     check_p2p_api(tmp_path, R)

@@ -18,7 +18,7 @@ KERNELS = [
     ("(a) pack_tab_kernel f32->f32", r"pack_tab_kernelILi1ELi1EE"),
     ("(b) sum_kernel f32 M=8", r"sum_kernelILi1ELi8EE"),
     ("(c) sgd_tab_kernel f32 momentum", r"sgd_tab_kernelILi1ELi1ELb1EE"),
-    ("(a)+(c) pack_sgd_tab_kernel f32 momentum (one rank)", r"pack_sgd_tab_kernelILi1ELi1ELi1ELb1EE"),
+    ("(a)+(c) pack_sgd_tab_kernel f32 momentum (one rank)", r"pack_sgd_tab_kernelILi1ELi1ELi1ELb1ELi1EE"),
     ("(b)+(c) p2p_allreduce_kernel f32 update momentum M=4", r"p2p_allreduce_kernelILi1ELi1ELb1ELb1ELi4ELb0EE"),
     ("(b)+(c) p2p_zero_kernel f32 momentum M=4 (ZeRO-1)", r"p2p_zero_kernelILi1ELi1ELb1ELi4EE"),
 ]
