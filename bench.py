@@ -222,7 +222,7 @@ class Clocks:
 
 
 # committed `ncu --set full` captures of the N=1 headline workload, newest first
-NCU_CAPTURES = ("r2", "r1b")  # newest first
+NCU_CAPTURES = ("r2f", "r2", "r1b")  # newest first
 
 
 def ncu_traffic(kernel: str):
@@ -623,6 +623,13 @@ def main():
         achieved = bytes_launch / avg_s / 1e9 if avg_s > 0 else 0.0
         traffic = (ncu_traffic(f"{dom}_tab_kernel") if (bound == "hbm" and args.config == "resnet50"
                                                        and bucket_mb == 100 and world == 1) else None)
+        if bound == "nvlink":
+            # 770 is the one-way peer copy; an allreduce loads every link both
+            # ways, where tools/nvlink_probe.cu measures this pool's ceiling
+            ceil = {2: 692.5, 4: 581.2}.get(world)
+            ceiling = ({"gbs": ceil, "frac": round(achieved / ceil, 4),
+                        "source": f"profiles/r2_nvlink_probe_n{world}.txt: best all-to-all pattern "
+                                  "(copy engines, every GPU sending and receiving)"} if ceil else None)
         line["roofline"] = {"bound": bound, "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                             "unit": "GB/s", "frac": round(achieved / peak, 4),
                             "traffic": traffic["bytes"] if traffic else None,
@@ -631,6 +638,7 @@ def main():
                             "avg_launch_us": round(1000 * ks["total_ms"] / max(1, ks["launches"]), 2),
                             "bytes_per_launch": round(bytes_launch),
                             "peak_source": peak_source,
+                            **({"all_to_all_ceiling": ceiling} if bound == "nvlink" else {}),
                             "kernels": {k: {"launches": v["launches"],
                                             "ms_per_step": round(v["total_ms"] / n_prof, 4),
                                             "GBps": round(v["bytes"] / (v["total_ms"] * 1e6), 1) if v["total_ms"] else None}

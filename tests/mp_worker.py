@@ -36,7 +36,7 @@ def t64(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
 
 
-def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False):
+def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False, shared_comms=None):
     """One rank of `case` on transport `tr` (NCCL across processes, or a local
     peer transport shared by rank threads on one GPU when colocated).  Writes
     the rank's .npz; returns the rank's JSON record."""
@@ -66,7 +66,10 @@ def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False):
         sizes = [int(x) for x in gold["sizes"]]
         K, lr, rescale = len(sizes), float(gold["lr"]), 1.0 / (64 * world)
         outstanding = 2 if mode == "concom" else 1
-        comms = create_communicators(tr, outstanding) if mode == "concom" else []
+        # colocated rank threads share ONE transport: its communicators are
+        # created once for all of them (run_colocated), not once per rank
+        comms = ((shared_comms if shared_comms is not None else create_communicators(tr, outstanding))
+                 if mode == "concom" else [])
         eng = Engine(4, rank, sink, local)
         cfg = KvConfig(mode, outstanding, K, bucket_bytes=16 * 1024 if p2p else 0, p2p=int(p2p), zero=int(zero))
         store = KvStore(eng, tr, rank, cfg, comms)
@@ -341,6 +344,7 @@ def run_colocated(case, world, outdir, watchdog_ms=60000):
     assert tr.p2p_capable()
     outs, errs = [None] * world, []
     dev = torch.device("cuda", 0)
+    shared_comms = create_communicators(tr, 2) if case.split("_")[0] == "concom" else None
 
     def body(r):
         try:
@@ -348,7 +352,7 @@ def run_colocated(case, world, outdir, watchdog_ms=60000):
             # every rank thread on its own framework stream: a rank's torch work
             # must never queue behind another rank's wait on a peer kernel
             with torch.cuda.stream(torch.cuda.Stream(dev)):
-                outs[r] = run_rank(case, r, world, tr, dev, outdir, sink, colocated=True)
+                outs[r] = run_rank(case, r, world, tr, dev, outdir, sink, colocated=True, shared_comms=shared_comms)
         except BaseException as e:  # re-raised on the caller's thread
             errs.append(e)
 
