@@ -475,6 +475,8 @@ def main():
         args.backward_ms if args.backward_ms is not None else bwd_spec, keys)
     config = config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world)
     if args.comm is None:  # the fused kernel needs fusion buckets and one communicator stream
+        # ConCom keeps NCCL: its concurrent peer-memory kernels (grids capped to
+        # co-reside) measured faster at 2 GPUs but slower at 4
         args.comm = "nccl" if (mode == "concom" or not bucket_mb) else "p2p"
     zero_on = args.zero and args.comm == "p2p" and mode == "depcha" and dtype == "fp32" and world > 1
 
@@ -521,7 +523,10 @@ def main():
                   direct_grads=direct_active(args, mode, bucket_mb, world))
     path = {"collectives": ("identity (1 rank)" if world == 1 else
                             {"nccl": "NCCL" + (f", {outstanding} concurrent communicators" if concom else ""),
-                             "p2p": "fused allreduce+update kernel over NVLink peer memory (rank-order sums)",
+                             "p2p": (f"{outstanding} concurrent peer-memory allreduce kernels over NVLink (one per "
+                                     "communicator, grids capped to co-reside; rank-order sums) + separate update"
+                                     if concom else
+                                     "fused allreduce+update kernel over NVLink peer memory (rank-order sums)"),
                              "nvls": "fused allreduce+update kernel, NVSwitch multicast in-switch reduction"}[args.comm]),
             "optimizer_state": ("ZeRO-1: master weights + momentum sharded 1/N, weights all-gathered in the "
                                 "fused kernel" if zero_on else "replicated on every rank")}
@@ -653,8 +658,8 @@ def main():
             if sched == "concom":
                 if not comms_sched:
                     continue
-                kw = {**common, "mode": "concom", "outstanding": sched_outstanding, "p2p": 0, "zero": False,
-                      "bucket_bytes": 25 << 20}
+                kw = {**common, "mode": "concom", "outstanding": sched_outstanding, "zero": False, "p2p": 0,
+                      "bucket_bytes": 25 << 20, "direct_grads": False}
                 coll = (f"NCCL, {sched_outstanding} communicators, 25 MiB buckets" if world > 1 else
                         f"identity (1 rank), {sched_outstanding} communicators, 25 MiB buckets")
                 cc = comms_sched

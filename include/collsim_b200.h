@@ -234,7 +234,10 @@ typedef struct cs_kv_config {
   int comm_priority;     /* CUDA stream priority of the comm lanes (<=0, lower = higher prio) */
   int p2p;               /* 1: NVLink peer-memory collectives (needs bucket_bytes > 0 and a
                             peer-capable NCCL transport); DepCha pull_update becomes one fused
-                            allreduce+update kernel per bucket, rank-order (bit-exact) sums */
+                            allreduce+update kernel per bucket, rank-order (bit-exact) sums;
+                            ConCom runs one peer-memory allreduce per communicator concurrently,
+                            each grid capped to 1/outstanding of the device so all co-reside.
+                            2: NVSwitch multicast (NVLS, funnel/depcha only) */
   int zero;              /* 1 (DepCha, p2p = 1): ZeRO-1 -- each rank keeps master weights and momentum of
                             its shard only; the fused kernel reduce-scatters, updates the shard and
                             all-gathers the weights.  pull_update must cover whole buckets. */

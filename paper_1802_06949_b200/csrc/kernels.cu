@@ -2074,15 +2074,16 @@ uint64_t p2p_shard_elems(uint64_t count, int nranks) {
 // (every rank's grid on one device, local peer transport) share the SMs:
 // each grid gets at most 1/nranks of the device's resident 512-thread CTAs,
 // so all nranks grids are resident at once and the pair barriers can meet.
-int p2p_grid(uint64_t groups, int nranks, bool colocated) {
+int p2p_grid(uint64_t groups, int nranks, bool colocated, int concurrent) {
   static const uint64_t cap = [] {
     const char* e = std::getenv("CSB_P2P_CTAS");  // identical on every rank (same environment)
     return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 148);
   }();
   uint64_t limit = std::min<uint64_t>(cap, kP2PMaxCtas);
-  if (colocated) {
+  if (colocated || concurrent > 1) {
     const uint64_t resident = static_cast<uint64_t>(sm_count_for_current_device()) * 2;  // __launch_bounds__(512, 2)
-    limit = std::min<uint64_t>(limit, std::max<uint64_t>(1, resident / static_cast<uint64_t>(nranks)));
+    const uint64_t share = static_cast<uint64_t>(colocated ? nranks : 1) * static_cast<uint64_t>(std::max(1, concurrent));
+    limit = std::min<uint64_t>(limit, std::max<uint64_t>(1, resident / share));
   }
   const uint64_t per_rank = groups / static_cast<uint64_t>(nranks);
   const uint64_t want = std::max<uint64_t>(1, per_rank / (2 * kP2PLinkThreads));
@@ -2139,7 +2140,7 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   }();
   p.piece = piece;
   p.timeout_ns = a.timeout_ns ? a.timeout_ns : p2p_timeout_ns();
-  const int grid = p2p_grid(p.groups, a.nranks, a.colocated);
+  const int grid = p2p_grid(p.groups, a.nranks, a.colocated, a.concurrent);
   const bool upd = a.update && a.tab && a.n_entries > 0;
   const bool mom = a.momentum != 0.0;
   const double elems = static_cast<double>(a.count);
@@ -2213,7 +2214,8 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
   p.sys_fence = fence;
   // colocated grids share one device: a cooperative launch would claim the
   // whole device per grid, so those launch plainly (p2p_grid keeps them co-resident)
-  if (coop && !a.colocated) CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
+  if (coop && !a.colocated && a.concurrent <= 1)
+    CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   else CSB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, s));
   ls.done();
 }

@@ -114,6 +114,12 @@ struct P2PArgs {
   // every rank's grid on the SAME device (local peer transport): cap each
   // grid so all `nranks` grids are co-resident, plain (non-cooperative) launch
   bool colocated = false;
+  // peer launches that may run at the same time on this device (ConCom's
+  // communicators): every grid is capped to 1/concurrent of the device's
+  // resident CTAs and launched plainly, so all of them can be resident at
+  // once on every GPU whatever order they start in -- none can hold the SMs
+  // a peer-waiting grid of another communicator needs
+  int concurrent = 1;
   // host-mapped abort word (device address): [0] code, [1..3] where.  The
   // pair barriers poll it while waiting and give up (no __trap) once it is
   // set, or set it themselves after `timeout_ns` without the peer.
@@ -125,7 +131,7 @@ enum : uint32_t { kAbortNone = 0, kAbortHost = 1, kAbortDeviceTimeout = 2 };
 size_t p2p_flag_bytes();
 // elements of the largest shard of a `count`-element bucket (a multiple of 8)
 uint64_t p2p_shard_elems(uint64_t count, int nranks);
-int p2p_grid(uint64_t groups, int nranks, bool colocated = false);
+int p2p_grid(uint64_t groups, int nranks, bool colocated = false, int concurrent = 1);
 void p2p_allreduce(const P2PArgs& args, cudaStream_t s);
 // CSB_P2P_TIMEOUT_MS (default 30000): a pair barrier waiting longer than this
 // for a peer CTA records kAbortDeviceTimeout and the kernel returns

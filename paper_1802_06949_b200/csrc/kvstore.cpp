@@ -67,11 +67,13 @@ KvStore::KvStore(Engine& engine, Transport& transport, int rank, KvConfig config
   comm_dt_ = cfg_.comm_dtype;
   if (cfg_.p2p && cfg_.bucket_bytes == 0)
     throw ConfigError("KvStore: the peer-memory path needs fusion buckets (bucket_bytes > 0)");
-  // Peer kernels pair CTAs across GPUs and are cooperative-launched; two of
-  // them on concurrent streams of one GPU (ConCom's communicators) could each
-  // hold the SMs the other needs on a peer, so ConCom stays on NCCL.
-  if (cfg_.p2p && cfg_.mode == KvMode::ConCom)
-    throw ConfigError("KvStore: the peer-memory path runs on one ordered comm stream (funnel/depcha)");
+  // Peer kernels pair CTAs across GPUs.  ConCom runs up to `outstanding` of
+  // them concurrently (one per communicator stream): each grid is capped to
+  // 1/outstanding of the device's resident CTAs and launched plainly, so all
+  // of them are resident together and none can hold the SMs that another
+  // communicator's peer-waiting grid needs (P2PArgs::concurrent).
+  if (cfg_.p2p == 2 && cfg_.mode == KvMode::ConCom)
+    throw ConfigError("KvStore: NVLS runs on one ordered comm stream (funnel/depcha)");
   // ZeRO-1 lives in DepCha's fused pull (Funnel/ConCom issue the collective
   // at push, before the weights are known)
   if (cfg_.zero && (cfg_.p2p != 1 || cfg_.mode != KvMode::DepCha))
@@ -525,7 +527,7 @@ void KvStore::collective_body(const Bucket& B, int b, cudaStream_t s, const Tran
   const int bid = cfg_.bucket_bytes ? b : -1;
   if (p2p_active_) {
     transport_.allreduce_p2p(B.comm, rank_, B.peer_bufs.data(), B.count, comm_dt_, B.keys[0], s, bid, upd,
-                             B.mc);
+                             B.mc, cfg_.mode == KvMode::ConCom ? cfg_.outstanding : 1);
   } else {
     transport_.allreduce_sum(B.comm, rank_, B.base, B.count, comm_dt_, B.keys[0], s, bid);
   }

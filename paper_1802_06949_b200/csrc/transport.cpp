@@ -342,7 +342,7 @@ void Transport::serialize_launch(int comm, int rank, cudaStream_t s, bool after)
 
 void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
                               int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
-                              void* mc) {
+                              void* mc, int concurrent) {
   if (!p2p_capable()) throw UsageError("Transport: peer-memory path unavailable");
   if (count == 0) throw UsageError("allreduce_sum: empty buffer");
   if (rank < 0 || rank >= num_ranks()) throw UsageError("collective: rank out of range");
@@ -384,6 +384,7 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   a.nranks = num_ranks();
   a.rank = rank;
   a.colocated = colocated();
+  a.concurrent = concurrent;
   a.abort_word = abort_dev_;
   a.count = count;
   a.cdt = dtype;

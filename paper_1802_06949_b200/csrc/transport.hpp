@@ -112,9 +112,11 @@ class Transport {
   // Allreduce of one bucket through peer memory, matched by the ledger like
   // allreduce_sum; with `upd`, fused with the SGD / momentum update of the
   // keys in the bucket (kernels.cu p2p_allreduce_kernel).
+  // `concurrent`: peer launches of other communicators that may run at the
+  // same time on this device (ConCom), see P2PArgs::concurrent.
   void allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
                      int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
-                     void* mc = nullptr);
+                     void* mc = nullptr, int concurrent = 1);
   // NVLink SHARP: every rank's device supports multicast objects.
   bool nvls_capable() const { return p2p_capable() && nvls_ok_; }
   // Setup-phase collective: a multicast-bound allocation (nvls.hpp).

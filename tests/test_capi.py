@@ -92,7 +92,7 @@ def test_kvstore_config_validation_before_any_device_work():
         (KvConfig("funnel", 1, 0), "num_keys"),
         (KvConfig("concom", 0, 4), "outstanding"),
         (KvConfig("depcha", 1, 4, p2p=1), "fusion buckets"),
-        (KvConfig("concom", 1, 4, bucket_bytes=1 << 20, p2p=1), "one ordered comm stream"),
+        (KvConfig("concom", 1, 4, bucket_bytes=1 << 20, p2p=2), "one ordered comm stream"),
         (KvConfig("funnel", 1, 4, bucket_bytes=1 << 20, p2p=1, zero=1), "ZeRO-1"),
         (KvConfig("depcha", 1, 4, bucket_bytes=1 << 20, zero=1), "ZeRO-1"),
     ]

@@ -40,7 +40,7 @@ def run_config(keys, R, *, mode, dtype, bucket_mb, peer, outstanding=1, zero=Fal
             m = api.SynthModel(eng, tr, r, R, keys, mode=mode, w_dtype=api.F32, g_dtype=D[dtype],
                                comm_dtype=D[dtype], bucket_bytes=int(bucket_mb * 2**20), issue_order=1,
                                outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * R), momentum=momentum,
-                               p2p=1 if (peer and mode != "concom") else 0, zero=zero, order_seed=order_seed,
+                               p2p=1 if peer else 0, zero=zero, order_seed=order_seed,
                                concom_comms=comms)
             m.init()
             m.run(3, m.BACKWARD | m.COMM)
@@ -78,12 +78,16 @@ def test_c2_resnet50_depcha_zero_fused_kernel(gpu):
     run_config(keys_of("resnet50"), 2, mode="depcha", dtype="fp32", bucket_mb=100, peer=True, zero=True)
 
 
-def test_c3_alexnet_concom_4_communicators(gpu):
-    run_config(keys_of("alexnet"), 2, mode="concom", dtype="fp32", bucket_mb=25, peer=False, outstanding=4)
+@pytest.mark.parametrize("peer", [False, True])
+def test_c3_alexnet_concom_4_communicators(gpu, peer):
+    """ConCom x 4 over the in-process transport (kernel (b)) and over the
+    peer-memory kernel (four communicators' grids concurrently, each capped
+    to a quarter of the device's share)."""
+    run_config(keys_of("alexnet"), 2, mode="concom", dtype="fp32", bucket_mb=25, peer=peer, outstanding=4)
 
 
 @pytest.mark.parametrize("mode,bucket_mb,peer", [("depcha", 128, True), ("funnel", 128, True),
-                                                 ("concom", 25, False)])
+                                                 ("concom", 25, True)])
 def test_c4_resnet152_bf16_all_schedules(gpu, mode, bucket_mb, peer):
     run_config(keys_of("resnet152"), 2, mode=mode, dtype="bf16", bucket_mb=bucket_mb, peer=peer,
                outstanding=4 if mode == "concom" else 1)

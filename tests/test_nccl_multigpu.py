@@ -76,13 +76,16 @@ def test_nccl_schedules_match_reference(two_gpus, tmp_path, mode):
         check_schedule_weights(d, mode, mode, R, outs, exact=(R == 2))
 
 
-@pytest.mark.parametrize("mode,variant", [("depcha", "p2p"), ("funnel", "p2p"), ("depcha", "p2pzero")])
+@pytest.mark.parametrize("mode,variant", [("depcha", "p2p"), ("funnel", "p2p"), ("depcha", "p2pzero"),
+                                          ("concom", "p2p")])
 def test_p2p_fused_allreduce_update_bit_exact(two_gpus, tmp_path, mode, variant):
     """DepCha / Funnel over the NVLink peer-memory path: one fused
     allreduce+SGD kernel per bucket (16 KiB fusion buckets).  Rank-order sums
     make the result bit-identical to the reference KvStore at every world
     size.  p2pzero: ZeRO-1 (each rank updates master weights of its shard
-    only, then the kernel all-gathers the weights) -- still bit-identical."""
+    only, then the kernel all-gathers the weights) -- still bit-identical.
+    concom: two communicators' peer kernels running concurrently, each grid
+    capped to half the device so both are always co-resident."""
     case = f"{mode}_{variant}"
     for R in world_sizes(two_gpus):
         d = tmp_path / f"R{R}"

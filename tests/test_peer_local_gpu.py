@@ -28,7 +28,7 @@ RANKS = [2, 4, 8]
 
 @pytest.mark.parametrize("R", RANKS)
 @pytest.mark.parametrize("mode,variant", [("depcha", "p2p"), ("funnel", "p2p"), ("depcha", "p2pzero"),
-                                          ("depcha", "p2psplit")])
+                                          ("depcha", "p2psplit"), ("concom", "p2p")])
 def test_colocated_fused_kernel_matches_reference_weights(gpu, tmp_path, R, mode, variant):
     case = f"{mode}_{variant}"
     outs = run_colocated(case, R, tmp_path)
