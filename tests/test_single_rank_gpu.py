@@ -82,3 +82,50 @@ def test_other_uses_of_the_bucket_see_the_staged_gradient(gpu):
     store.close()
     eng.close()
     tr.close()
+
+
+@pytest.mark.parametrize("R", [1, 2, 4])
+def test_e2e_host_upload_double_buffered_gives_the_device_run_weights(gpu, R):
+    """The e2e path (bench `e2e`): every step uploads the gradients from
+    pinned host memory into one of two device buffers, so step t+1's upload
+    overlaps step t's aggregation.  Weights after 5 steps must equal the
+    device-resident run's bit for bit -- at one rank (fused pack + update) and
+    over the colocated peer kernel (ZeRO-1, direct reads of the registered
+    double buffer, whose layout alternates between steps)."""
+    import threading
+    from paper_1802_06949_b200 import Engine, Transport, api
+    sizes = [1, 7, 64, 300, 4097, 70000]
+    tr = Transport.local(R, 60000, None, peer=R > 1)
+    out, errs = [None] * R, []
+
+    def rank(r):
+        try:
+            eng = Engine(4, r, None, 0)
+            kw = dict(mode="depcha", bucket_bytes=1 << 20, issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=0.9,
+                      p2p=R > 1, zero=R > 1, direct_grads=R > 1)
+            m1 = api.SynthModel(eng, tr, r, R, sizes, host_source=True, **kw)
+            m1.init()
+            m1.run_e2e(5, m1.BACKWARD | m1.COMM)
+            w1 = m1.read_weights()
+            m1.close()
+            m2 = api.SynthModel(eng, tr, r, R, sizes, **kw)
+            m2.init()
+            m2.run(5, m2.BACKWARD | m2.COMM)
+            w2 = m2.read_weights()
+            m2.close()
+            out[r] = (w1, w2)
+            eng.close()
+        except BaseException as e:
+            errs.append(e)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    tr.close()
+    if errs:
+        raise errs[0]
+    for r in range(R):
+        np.testing.assert_array_equal(out[r][0], out[r][1])
+        np.testing.assert_array_equal(out[r][0], out[0][0])
