@@ -129,10 +129,9 @@ void SynthModel::init() {
   });
   engine_.bind_device();
   CSB_CUDA(cudaMalloc(&w_arena_, wtot));
-  dbuf_ = cfg_.host_source && !cfg_.grad_views;
-  CSB_CUDA(cudaMalloc(&g_arena_, dbuf_ ? 2 * gtot : gtot));
+  CSB_CUDA(cudaMalloc(&g_arena_, gtot));
   CSB_CUDA(cudaMemcpy(w_arena_, wh.data(), wtot, cudaMemcpyHostToDevice));
-  CSB_CUDA(cudaMemset(g_arena_, 0, dbuf_ ? 2 * gtot : gtot));
+  CSB_CUDA(cudaMemset(g_arena_, 0, gtot));
   if (cfg_.host_source) {
     CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&src_arena_), gtot, cudaHostAllocDefault));
     std::memcpy(src_arena_, gh.data(), gtot);
@@ -179,10 +178,6 @@ void SynthModel::init() {
     src_.push_back(src_arena_ + goff[k]);
     wt_.push_back(engine_.new_variable());
     gt_.push_back(engine_.new_variable());
-    if (dbuf_) {
-      g2_.push_back(g_arena_ + gtot + goff[k]);
-      gt2_.push_back(engine_.new_variable());
-    }
   }
   sum_tag_[0] = engine_.new_variable();
   sum_tag_[1] = engine_.new_variable();
@@ -191,7 +186,7 @@ void SynthModel::init() {
   engine_.wait_all();
   groups_ = kv_.bucket_groups();
   h2d_dst_ = g_arena_;
-  if (cfg_.direct_grads && !cfg_.grad_views) kv_.register_grads(g_arena_, dbuf_ ? 2 * gtot : gtot);
+  if (cfg_.direct_grads && !cfg_.grad_views) kv_.register_grads(g_arena_, gtot);
   if (cfg_.grad_views) {
     if (cfg_.bucket_bytes == 0) throw ConfigError("synth: bucket views need fusion buckets");
     if (kv_.comm_dtype() != cfg_.gdt) throw ConfigError("synth: bucket views need comm dtype == gradient dtype");
@@ -220,13 +215,12 @@ void SynthModel::init() {
 void SynthModel::enqueue_step(int flags) {
   const int K = static_cast<int>(cfg_.sizes.size());
   const int gdt = cfg_.gdt;
-  if (dbuf_ && (flags & kStepBackward)) buf_ ^= 1;  // a new upload goes to the other buffer
-  const std::vector<void*>& G = buf_ ? g2_ : g_;
-  const std::vector<Tag>& GT = buf_ ? gt2_ : gt_;
+  const std::vector<void*>& G = g_;
+  const std::vector<Tag>& GT = gt_;
   if ((flags & kStepBackward) && cfg_.host_source) {
     // e2e input upload: the step's gradients arrive from pinned host memory
     // in one H2D copy of the contiguous gradient arena
-    void* dst = static_cast<char*>(h2d_dst_) + (buf_ ? g_arena_bytes_ : 0);
+    void* dst = h2d_dst_;
     const void* src = src_arena_;
     const size_t bytes = g_arena_bytes_;
     engine_.push_stream(

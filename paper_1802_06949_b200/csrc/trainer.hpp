@@ -85,13 +85,6 @@ class SynthModel {
   KvStore kv_;
   std::vector<void*> w_, g_, src_;
   std::vector<Tag> wt_, gt_;
-  // e2e (host_source): a second gradient buffer, so step t+1's upload runs
-  // while step t's aggregation still reads buffer t % 2 (a data loader's
-  // prefetch); buf_ = the buffer the current step uses
-  bool dbuf_ = false;
-  int buf_ = 0;
-  std::vector<void*> g2_;
-  std::vector<Tag> gt2_;
   std::vector<uint64_t> spin_ns_;
   std::vector<int> produce_order_;  // producer order (descending keys or measured ready order)
   char* w_arena_ = nullptr;

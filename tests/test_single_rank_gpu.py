@@ -85,13 +85,13 @@ def test_other_uses_of_the_bucket_see_the_staged_gradient(gpu):
 
 
 @pytest.mark.parametrize("R", [1, 2, 4])
-def test_e2e_host_upload_double_buffered_gives_the_device_run_weights(gpu, R):
+def test_e2e_host_upload_gives_the_device_run_weights(gpu, R):
     """The e2e path (bench `e2e`): every step uploads the gradients from
-    pinned host memory into one of two device buffers, so step t+1's upload
-    overlaps step t's aggregation.  Weights after 5 steps must equal the
-    device-resident run's bit for bit -- at one rank (fused pack + update) and
-    over the colocated peer kernel (ZeRO-1, direct reads of the registered
-    double buffer, whose layout alternates between steps)."""
+    pinned host memory through the C ABI.  Weights after 5 steps must equal
+    the device-resident run's bit for bit -- at one rank (fused pack + update)
+    and over the colocated peer kernel (ZeRO-1, direct reads of the registered
+    upload buffer).  (A double-buffered upload was measured and dropped: the
+    step is host-link bound, 2.05 ms of H2D per 102 MB either way.)"""
     import threading
     from paper_1802_06949_b200 import Engine, Transport, api
     sizes = [1, 7, 64, 300, 4097, 70000]
