@@ -934,6 +934,7 @@ struct P2PParams {
   int pack;       // stage the gradients (entry d) into this rank's bucket (entry a) before barrier 0
   uint32_t epoch;
   uint64_t piece;  // groups per piece of the interleaved CTA map (0: one contiguous range per CTA)
+  uint64_t kmin;   // at least this many pieces per CTA when each would still hold >= 256 groups
   // direct: phase 1 reads every rank's gradients in place -- rank r's copy of
   // entry e is gbase[r] + (e.d - gbase[rank]) (registered regions, identical
   // layout on every rank) -- instead of staged bucket copies; nothing is packed
@@ -954,7 +955,8 @@ template <typename F>
 __device__ __forceinline__ void for_pieces(const P2PParams& p, int s, F&& f) {
   const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
   const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
-  const uint64_t K = p.piece ? max(static_cast<uint64_t>(1), L / (G * p.piece)) : 1;
+  uint64_t K = p.piece ? max(static_cast<uint64_t>(1), L / (G * p.piece)) : 1;
+  if (p.piece && K < p.kmin && L / (G * p.kmin) >= 256) K = p.kmin;
   const uint64_t P = G * K;
   for (uint64_t k = 0; k < K; ++k) {
     const uint64_t i = c + k * G;
@@ -2139,6 +2141,11 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     return static_cast<uint64_t>(e ? std::max(0, std::atoi(e)) : 4096);
   }();
   p.piece = piece;
+  static const uint64_t kmin = [] {
+    const char* e = std::getenv("CSB_P2P_KMIN");  // identical on every rank (same environment)
+    return static_cast<uint64_t>(e ? std::max(1, std::atoi(e)) : 1);
+  }();
+  p.kmin = kmin;
   p.timeout_ns = a.timeout_ns ? a.timeout_ns : p2p_timeout_ns();
   const int grid = p2p_grid(p.groups, a.nranks, a.colocated, a.concurrent);
   const bool upd = a.update && a.tab && a.n_entries > 0;
