@@ -195,6 +195,13 @@ int cs_transport_share_buffer_rank(cs_transport_t t, int rank, void* base, void*
  * barrier records where it waited and the kernel returns -- no __trap) or an
  * NCCL asynchronous error, as text into buf ("" when healthy) */
 int cs_transport_device_failure(cs_transport_t t, char* buf, int cap);
+/* CSB_P2P_TRACE=1 (set before the transport is created): the last peer
+ * launch of `rank` stamps %globaltimer per CTA at 5 points -- start, past
+ * the arrival barrier, own shard done, past barrier 1, end -- into
+ * host-mapped memory; copies up to `cap` values (CTA-major) into out, *n =
+ * the total (0 when tracing is off).  A diagnostic for the peer kernels,
+ * which ncu cannot replay (their CTAs wait on other GPUs). */
+int cs_transport_p2p_stamps(cs_transport_t t, int rank, uint64_t* out, int cap, int* n);
 /* allreduce of peer_bufs[*] (n elements, multiple of 8) in rank order, every
  * rank ends with the sum.  Launches of one (comm, rank) run in call order even
  * on different streams (they share the comm's flag region); every rank must

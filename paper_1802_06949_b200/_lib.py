@@ -107,6 +107,7 @@ SIGNATURES = {
     "cs_transport_share_buffer": [_P, _P, C.POINTER(_P)],
     "cs_transport_share_buffer_rank": [_P, _I, _P, C.POINTER(_P)],
     "cs_transport_device_failure": [_P, C.c_char_p, _I],
+    "cs_transport_p2p_stamps": [_P, _I, C.POINTER(C.c_uint64), _I, C.POINTER(_I)],
     "cs_allreduce_p2p": [_P, _I, _I, C.POINTER(_P), _U64, _I, _I, C.c_void_p, _P],
     "cs_transport_nvls_capable": [_P, _PI],
     "cs_transport_alloc_nvls": [_P, _U64, C.POINTER(_P), C.POINTER(_P)],

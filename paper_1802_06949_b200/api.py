@@ -381,6 +381,18 @@ class Transport:
             check(lib.cs_transport_share_buffer_rank(self.h, rank, base, out))
         return [p or 0 for p in out]
 
+    def p2p_stamps(self, rank: int):
+        """CSB_P2P_TRACE=1: the last peer launch's per-CTA phase stamps of
+        `rank` as a (CTAs, 5) uint64 array (ns; rows of unused CTAs are 0)."""
+        import numpy as np
+        n = C.c_int()
+        check(lib.cs_transport_p2p_stamps(self.h, rank, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint64)
+        if n.value:
+            check(lib.cs_transport_p2p_stamps(self.h, rank, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value,
+                                              C.byref(n)))
+        return out.reshape(-1, 5)
+
     def device_failure(self) -> str:
         """A peer kernel's device timeout or an NCCL asynchronous error ("" if none)."""
         buf = C.create_string_buffer(512)

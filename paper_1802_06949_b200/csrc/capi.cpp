@@ -411,6 +411,15 @@ int cs_transport_device_failure(cs_transport_t t, char* buf, int cap) {
     }
   });
 }
+int cs_transport_p2p_stamps(cs_transport_t t, int rank, uint64_t* out, int cap, int* n) {
+  return guard([&] {
+    CHECK_HANDLE(t);
+    const std::vector<uint64_t> v = t->t->p2p_stamps(rank);
+    const int m = std::min(cap, static_cast<int>(v.size()));
+    if (m > 0) std::memcpy(out, v.data(), sizeof(uint64_t) * static_cast<size_t>(m));
+    if (n) *n = static_cast<int>(v.size());
+  });
+}
 namespace {
 struct P2PTables {  // resident tables of the C-ABI p2p entry point, per stream
   std::mutex mu;

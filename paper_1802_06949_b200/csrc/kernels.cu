@@ -940,7 +940,20 @@ struct P2PParams {
   // layout on every rank) -- instead of staged bucket copies; nothing is packed
   int direct;
   void* gbase[CS_MAX_RANKS];
+  // CSB_P2P_TRACE: per-CTA %globaltimer stamps of the launch's phases
+  // (kP2PStamps per CTA: start, past barrier 0, own shard done, past
+  // barrier 1, end), host-mapped; null = off
+  uint64_t* stamps;
 };
+
+constexpr int kP2PStamps = 5;
+__device__ __forceinline__ void p2p_stamp(const P2PParams& p, int i) {
+  if (p.stamps && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.stamps[static_cast<size_t>(blockIdx.x) * kP2PStamps + i] = t;
+  }
+}
 
 // CTA c's share of shard s: the shard is cut into G x K equal pieces
 // (K ~ L / (G x piece)), piece i to CTA i mod G -- interleaved like the
@@ -951,12 +964,20 @@ struct P2PParams {
 // CTA.  Default 4096 groups (128 KiB of fp32 per piece): ResNet-50 ZeRO-1
 // step at 2 GPUs 0.263 ms vs 0.397 contiguous, at 4 GPUs 0.340 vs 0.343;
 // small pieces (512) measured slower at 4 GPUs (0.427 ms).
+// pieces per CTA of shard s (host twin: p2p_pieces_per_cta)
+__device__ __forceinline__ uint64_t shard_k(const P2PParams& p, int s, uint64_t G) {
+  const uint64_t T = p.groups;
+  const uint64_t L = T * (s + 1) / p.nranks - T * s / p.nranks;
+  uint64_t K = p.piece ? max(static_cast<uint64_t>(1), L / (G * p.piece)) : 1;
+  if (p.piece && K < p.kmin && L / (G * p.kmin) >= 256) K = p.kmin;
+  return K;
+}
+
 template <typename F>
 __device__ __forceinline__ void for_pieces(const P2PParams& p, int s, F&& f) {
   const uint64_t T = p.groups, G = gridDim.x, c = blockIdx.x;
   const uint64_t s0 = T * s / p.nranks, L = T * (s + 1) / p.nranks - s0;
-  uint64_t K = p.piece ? max(static_cast<uint64_t>(1), L / (G * p.piece)) : 1;
-  if (p.piece && K < p.kmin && L / (G * p.kmin) >= 256) K = p.kmin;
+  const uint64_t K = shard_k(p, s, G);
   const uint64_t P = G * K;
   for (uint64_t k = 0; k < K; ++k) {
     const uint64_t i = c + k * G;
@@ -1276,10 +1297,12 @@ __device__ __forceinline__ void p2p_update_range(const P2PParams& p, int owner, 
 
 template <int CDT, int WDT, bool UPDATE, bool MOM, int M, bool NVLS = false>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __grid_constant__ P2PParams p) {
+  p2p_stamp(p, 0);
   if constexpr (UPDATE && !NVLS) {
     if (p.pack && !p.direct) p2p_pack_column<CDT>(p);
   }
   if (!pair_barrier(p, 0)) return;
+  p2p_stamp(p, 1);
   for_pieces(p, p.rank, [&](uint64_t, uint64_t a, uint64_t b) {
     if constexpr (NVLS) nvls_reduce_chunk<CDT>(p, a, b);
     else p2p_reduce_chunk<CDT, M>(p, a, b);
@@ -1293,7 +1316,10 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __g
     __syncthreads();
     update_shard(p.rank);
   }
+  __syncthreads();
+  p2p_stamp(p, 2);
   if (!pair_barrier(p, 1)) return;
+  p2p_stamp(p, 3);
   if constexpr (NVLS) asm volatile("fence.proxy.alias;" ::: "memory");
   if constexpr (UPDATE) {
     // the other shards, staggered so the ranks start on different owners
@@ -1301,6 +1327,8 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_allreduce_kernel(const __g
     // shard_only: owners may repack their buckets only after every reader is done
     if (p.shard_only) pair_barrier(p, 2);
   }
+  __syncthreads();
+  p2p_stamp(p, 4);
 }
 
 // ------------------------------------------------ ZeRO-1
@@ -1405,17 +1433,24 @@ __device__ __forceinline__ void zero_gather(const P2PParams& p, int s, uint64_t 
 
 template <int CDT, int WDT, bool MOM, int M>
 __global__ void __launch_bounds__(kP2PThreads, 2) p2p_zero_kernel(const __grid_constant__ P2PParams p) {
+  p2p_stamp(p, 0);
   if (p.pack && !p.direct) p2p_pack_column<CDT>(p);
   if (!pair_barrier(p, 0)) return;
+  p2p_stamp(p, 1);
   for_pieces(p, p.rank, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_reduce_update<CDT, WDT, MOM, M>(p, s0, a, b); });
   __syncthreads();
   // own shard: no need to wait for the peers
   for_pieces(p, p.rank, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_gather<WDT>(p, p.rank, s0, a, b); });
+  __syncthreads();
+  p2p_stamp(p, 2);
   if (!pair_barrier(p, 1)) return;
+  p2p_stamp(p, 3);
   for (int k = 1; k < p.nranks; ++k) {
     const int s = (p.rank + k) % p.nranks;
     for_pieces(p, s, [&](uint64_t s0, uint64_t a, uint64_t b) { zero_gather<WDT>(p, s, s0, a, b); });
   }
+  __syncthreads();
+  p2p_stamp(p, 4);
 }
 
 // ------------------------------------------------- synthetic backward
@@ -2136,6 +2171,8 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     if (!aligned16(a.gbase[r])) throw UsageError("p2p_allreduce: gradient region not 16-byte aligned");
   }
   p.abort_word = a.abort_word;
+  p.stamps = a.stamps;
+
   static const uint64_t piece = [] {
     const char* e = std::getenv("CSB_P2P_PIECE");  // identical on every rank (same environment)
     return static_cast<uint64_t>(e ? std::max(0, std::atoi(e)) : 4096);

@@ -125,6 +125,9 @@ struct P2PArgs {
   // set, or set it themselves after `timeout_ns` without the peer.
   uint32_t* abort_word = nullptr;
   uint64_t timeout_ns = 0;
+  // CSB_P2P_TRACE: per-CTA phase stamps of this launch (device address of
+  // kP2PMaxCtas x 5 host-mapped uint64), null = off
+  uint64_t* stamps = nullptr;
 };
 // Abort codes in abort_word[0]
 enum : uint32_t { kAbortNone = 0, kAbortHost = 1, kAbortDeviceTimeout = 2 };

@@ -15,6 +15,10 @@
 namespace csb {
 
 namespace {
+constexpr size_t kStampsPerRank = 1184 * 5;  // kP2PMaxCtas x the peer kernels' phase stamps
+}  // namespace
+
+namespace {
 
 [[noreturn]] void throw_nccl(ncclResult_t r, const char* what, ncclComm_t comm) {
   std::string msg = std::string(what) + ": " + ncclGetErrorString(r);
@@ -162,6 +166,12 @@ void Transport::setup_abort() {
                          cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(abort_host_, 0, 4 * sizeof(uint32_t));
   CSB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&abort_dev_), abort_host_, 0));
+  if (const char* e = std::getenv("CSB_P2P_TRACE"); e && std::string(e) == "1") {
+    const size_t bytes = sizeof(uint64_t) * kStampsPerRank * kLedgerMaxRanks;
+    CSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stamps_host_), bytes, cudaHostAllocMapped));
+    std::memset(stamps_host_, 0, bytes);
+    CSB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&stamps_dev_), stamps_host_, 0));
+  }
   watch_id_ = watch::add([this] { return async_failure(); }, [this](const std::string& why) { abort(why); });
 }
 
@@ -386,6 +396,7 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   a.colocated = colocated();
   a.concurrent = concurrent;
   a.abort_word = abort_dev_;
+  if (stamps_dev_) a.stamps = stamps_dev_ + static_cast<size_t>(rank) * kStampsPerRank;
   a.count = count;
   a.cdt = dtype;
   a.epoch = static_cast<uint32_t>(t.seq + 1);  // same matched sequence on every rank
@@ -446,6 +457,12 @@ void Transport::wait_colocated(int comm, int rank) {
   }
 }
 
+std::vector<uint64_t> Transport::p2p_stamps(int rank) const {
+  if (!stamps_host_ || rank < 0 || rank >= kLedgerMaxRanks) return {};
+  const volatile uint64_t* p = stamps_host_ + static_cast<size_t>(rank) * kStampsPerRank;
+  return std::vector<uint64_t>(p, p + kStampsPerRank);
+}
+
 Transport::~Transport() {
   if (watch_id_ >= 0) watch::remove(watch_id_);
   for (LaunchOrder& lo : launch_order_)
@@ -458,6 +475,7 @@ Transport::~Transport() {
     for (void* p : own_flags_) cudaFree(p);
   }
   if (abort_host_) cudaFreeHost(abort_host_);
+  if (stamps_host_) cudaFreeHost(stamps_host_);
   if (backend_ == Backend::Nccl) {
     const bool aborted = ledger_ && ledger_->latched();
     cudaSetDevice(device_);

@@ -117,6 +117,10 @@ class Transport {
   void allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64_t count, int dtype,
                      int trace_key, cudaStream_t stream, int bucket, const P2PUpdate* upd,
                      void* mc = nullptr, int concurrent = 1);
+  // CSB_P2P_TRACE=1: the last peer launch's per-CTA phase stamps of `rank`
+  // (%globaltimer ns; CTA-major, 5 per CTA: start, past barrier 0, own shard
+  // done, past barrier 1, end); empty when tracing is off.
+  std::vector<uint64_t> p2p_stamps(int rank) const;
   // NVLink SHARP: every rank's device supports multicast objects.
   bool nvls_capable() const { return p2p_capable() && nvls_ok_; }
   // Setup-phase collective: a multicast-bound allocation (nvls.hpp).
@@ -155,6 +159,9 @@ class Transport {
   std::vector<LaunchOrder> launch_order_;  // comm * kLedgerMaxRanks + rank
   uint32_t* abort_host_ = nullptr;         // [0] abort code, [1..3] where (host-mapped)
   uint32_t* abort_dev_ = nullptr;
+  // CSB_P2P_TRACE=1: per-rank phase stamps of the last peer launch (host-mapped)
+  uint64_t* stamps_host_ = nullptr;
+  uint64_t* stamps_dev_ = nullptr;
   int watch_id_ = -1;
   bool p2p_ok_ = false;
   bool nvls_ok_ = false;
