@@ -113,8 +113,8 @@ def parse():
                         "results; bf16 gradient sets keep the replicated update, whose all-gather moves bf16 "
                         "sums instead of fp32 weights)")
     p.add_argument("--no-direct", dest="direct", action="store_false",
-                   help="N>1, fused peer kernel: stage the gradients into the comm buckets (kvstore.cpp:109) "
-                        "instead of registering the gradient arena and reading every rank's gradients in place")
+                   help="stage the gradients into the comm buckets (kvstore.cpp:109) instead of registering the "
+                        "gradient arena and reading the gradients in place (every rank's over NVLink at N>1)")
     p.add_argument("--grad-views", action="store_true",
                    help="gradients produced in place in the comm buckets (gradient-as-bucket-view): "
                         "push copies nothing")
@@ -222,7 +222,7 @@ class Clocks:
 
 
 # committed `ncu --set full` captures of the N=1 headline workload, newest first
-NCU_CAPTURES = ("r2f", "r2", "r1b")  # newest first
+NCU_CAPTURES = ("r2g", "r2f", "r2", "r1b")  # newest first
 
 
 def ncu_traffic(kernel: str):
@@ -264,9 +264,10 @@ def workload(args):
 
 
 def direct_active(args, mode, bucket_mb, world) -> bool:
-    """In-place peer reads of registered gradients: N>1, the fused peer
-    kernel (DepCha / Funnel over fusion buckets), separate gradient tensors."""
-    return (world > 1 and args.direct and not args.grad_views and mode != "concom" and bool(bucket_mb)
+    """Registered gradients read in place (KvStore.register_grads), nothing
+    staged: at N>1 by the fused peer kernel over NVLink, at N=1 by the fused
+    pack + update kernel (DepCha / Funnel over fusion buckets)."""
+    return (args.direct and not args.grad_views and mode != "concom" and bool(bucket_mb)
             and args.comm in (None, "p2p"))
 
 
@@ -279,7 +280,8 @@ def config_dict(args, keys, mode, outstanding, dtype, bucket_mb, world) -> dict:
             "producer_order": "per-rank random (seeded)" if args.config == "stress" else "reverse key order",
             "grad_layout": "bucket views (produced in place; push copies nothing)" if args.grad_views
             else ("separate gradient tensors in one registered region (KvStore.register_grads): the fused "
-                  "kernel reads every rank's gradients in place over NVLink, nothing staged"
+                  "kernel reads the gradients in place (every rank's over NVLink at N>1), nothing staged "
+                  "into the comm buckets"
                   if direct_active(args, mode, bucket_mb, world) else
                   "separate gradient tensors (push packs them into the comm buckets, kvstore.cpp:109)"),
             "step": "push + allreduce + pull/SGD update over every key (trainer.cpp:112-141), no backward",

@@ -285,13 +285,15 @@ int cs_kv_key_map(cs_kvstore_t kv, int key, int* bucket, uint64_t* offset_elems)
  * cs_kv_arena: the one allocation holding every fusion bucket (to zero it). */
 int cs_kv_bucket_view(cs_kvstore_t kv, int key, void** ptr);
 int cs_kv_arena(cs_kvstore_t kv, void** base, uint64_t* bytes);
-/* Setup collective (every rank, same order; peer-memory path only, a no-op
- * otherwise): the allocation holding this rank's gradients -- a cudaMalloc
- * base, keys at the same offsets on every rank.  A whole-bucket
- * cs_kv_pull_update whose pushed gradients all lie inside it makes the fused
- * peer kernel read every rank's gradients in place (nothing is staged into
- * the buckets; replaces the kvstore.cpp:109 copy).  Ranks whose layouts
- * differ fail with CS_ERR_MISMATCH before any launch. */
+/* Setup collective (every rank, same order): the allocation holding this
+ * rank's gradients -- any device pointer into it, keys at the same offsets
+ * on every rank.  A whole-bucket cs_kv_pull_update whose pushed gradients all
+ * lie inside it reads them in place and stages nothing into the buckets
+ * (replaces the kvstore.cpp:109 copy): at N > 1 the fused peer kernel reads
+ * every rank's gradients over NVLink, at one rank the fused pack + update
+ * kernel skips the staging store.  The buckets then hold no copy of those
+ * gradients afterwards (cs_kv_comm_buf), as under ZeRO-1.  Ranks whose
+ * layouts differ fail with CS_ERR_MISMATCH before any launch. */
 int cs_kv_register_grads(cs_kvstore_t kv, void* base, uint64_t bytes);
 int cs_kv_num_buckets(cs_kvstore_t kv, int* out);
 int cs_kv_bucket_lane(cs_kvstore_t kv, int bucket, int* lane);

@@ -725,14 +725,19 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
     }
     if (fuse) {
       // (a)+(c) in one op after the (identity) collective: reads the pushed
-      // gradients, writes the bucket and the weights
+      // gradients, writes the bucket and the weights.  Registered gradients
+      // (register_grads) are read in place and not staged into the bucket
+      // either -- the one-rank twin of the peer kernels' direct reads: the
+      // bucket then keeps no copy of this step's gradients (as under ZeRO-1).
+      const bool in_place = deferred_in_region(B);
       std::vector<DeviceTable::PackUpdate> pu;
       for (int i : idxs) {
         const int k = keys[static_cast<size_t>(i)];
         const TensorSlot& o = outs[static_cast<size_t>(i)];
         const void* g = key_ptr(k);  // a bucket view: already in place
         if (const void* src = deferred_src(k)) g = src;
-        pu.push_back(DeviceTable::PackUpdate{g, key_ptr(k), o.data, keys_[static_cast<size_t>(k)].mom, o.numel});
+        void* slot = in_place ? const_cast<void*>(g) : key_ptr(k);  // slot == g: no staging store
+        pu.push_back(DeviceTable::PackUpdate{g, slot, o.data, keys_[static_cast<size_t>(k)].mom, o.numel});
       }
       std::vector<Tag> reads;
       for (const Tag& t : B.deferred_reads)
@@ -773,14 +778,26 @@ void KvStore::pull_impl(const std::vector<int>& keys, const std::vector<TensorSl
 // unmodified until every rank has read them).
 void KvStore::register_grads(void* base, uint64_t bytes) {
   if (!base || bytes == 0) throw UsageError("KvStore: empty gradient region");
-  if (!p2p_active_) return;  // one rank, or NCCL: staging is the only form
-  if (!greg_peers_.empty()) throw UsageError("KvStore: a gradient region is already registered");
+  if (greg_base_) throw UsageError("KvStore: a gradient region is already registered");
+  greg_base_ = base;
+  greg_bytes_ = bytes;
+  if (!p2p_active_) return;  // one rank: the fused pull reads the region in place (no peers to map)
   engine_.bind_device();
   std::vector<void*> peers = transport_.share_buffer(base, rank_);
   shared_.push_back(peers);
-  greg_base_ = base;
-  greg_bytes_ = bytes;
   greg_peers_.assign(peers.begin(), peers.end());
+}
+
+// every deferred gradient of B lies in the registered region (16-B aligned)
+bool KvStore::deferred_in_region(const Bucket& B) const {
+  if (!greg_base_ || B.deferred.empty()) return false;
+  const char* base = static_cast<const char*>(greg_base_);
+  const size_t es = dtype_size(B.deferred_dt < 0 ? comm_dt_ : B.deferred_dt);
+  for (const auto& [k, e] : B.deferred) {
+    const char* d = static_cast<const char*>(e.src);
+    if (d < base || d + e.n * es > base + greg_bytes_ || (reinterpret_cast<uintptr_t>(d) & 15u) != 0) return false;
+  }
+  return true;
 }
 
 // kvstore.cpp:185-193: drain the in-flight counter, then a world barrier.

@@ -112,8 +112,9 @@ class KvStore {
   // the collective then rewrites it in place.  Builds the buckets.
   void* bucket_view(int key);
   // Setup collective: register the allocation holding this rank's gradients
-  // (a cudaMalloc base, same layout on every rank) so the fused peer kernel
-  // reads them in place instead of staging them into the buckets.
+  // (same layout on every rank) so the fused kernels read them in place
+  // instead of staging them into the buckets (N > 1: over NVLink from every
+  // peer; one rank: the fused pack+update kernel skips the staging store).
   void register_grads(void* base, uint64_t bytes);
   // The fusion-bucket arena (one allocation holding every bucket).
   void arena(void** base, uint64_t* bytes);
@@ -188,6 +189,7 @@ class KvStore {
   void* greg_base_ = nullptr;
   uint64_t greg_bytes_ = 0;
   std::vector<const void*> greg_peers_;
+  bool deferred_in_region(const Bucket& B) const;
   const void* deferred_src(int k) const {
     return static_cast<size_t>(k) < defer_src_.size() ? defer_src_[static_cast<size_t>(k)] : nullptr;
   }

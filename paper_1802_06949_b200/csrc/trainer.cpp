@@ -186,7 +186,7 @@ void SynthModel::init() {
   engine_.wait_all();
   groups_ = kv_.bucket_groups();
   h2d_dst_ = g_arena_;
-  if (cfg_.direct_grads && !cfg_.grad_views) kv_.register_grads(g_arena_, gtot);
+  if (cfg_.direct_grads && !cfg_.grad_views) kv_.register_grads(g_arena_, gtot);  // any N
   if (cfg_.grad_views) {
     if (cfg_.bucket_bytes == 0) throw ConfigError("synth: bucket views need fusion buckets");
     if (kv_.comm_dtype() != cfg_.gdt) throw ConfigError("synth: bucket views need comm dtype == gradient dtype");

@@ -18,14 +18,18 @@ SIZES = [1, 7, 64, 300, 4097, 70000, 1 << 18]
 @pytest.mark.parametrize("wdt,gdt,cdt,mu", [("f32", "f32", "f32", 0.9), ("f32", "f32", "f32", 0.0),
                                             ("f32", "bf16", "bf16", 0.9), ("f32", "f32", "bf16", 0.9),
                                             ("f64", "f64", "f64", 0.0), ("f64", "f64", "f64", 0.9)])
-@pytest.mark.parametrize("bucket_bytes", [1 << 20, 0])
-def test_fused_pack_update_matches_oracle(gpu, wdt, gdt, cdt, mu, bucket_bytes):
+@pytest.mark.parametrize("bucket_bytes,direct", [(1 << 20, False), (0, False), (1 << 20, True)])
+def test_fused_pack_update_matches_oracle(gpu, wdt, gdt, cdt, mu, bucket_bytes, direct):
+    """direct: the gradient arena is registered (KvStore.register_grads), so
+    the fused kernel reads the gradients in place and skips the staging store
+    (when the gradient dtype is the comm dtype) -- same weights."""
     from paper_1802_06949_b200 import Engine, Transport, api
     D = {"f64": api.F64, "f32": api.F32, "bf16": api.BF16}
     tr = Transport.local(1, 10000)
     eng = Engine(2, 0, None, 0)
     m = api.SynthModel(eng, tr, 0, 1, SIZES, mode="depcha", w_dtype=D[wdt], g_dtype=D[gdt], comm_dtype=D[cdt],
-                       bucket_bytes=bucket_bytes, issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=mu)
+                       bucket_bytes=bucket_bytes, issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=mu,
+                       direct_grads=direct)
     m.init()
     nb = m.info()["num_buckets"]
     api.profile_reset()
@@ -33,6 +37,7 @@ def test_fused_pack_update_matches_oracle(gpu, wdt, gdt, cdt, mu, bucket_bytes):
     m.run(3, m.BACKWARD | m.COMM)
     api.profile_enable(False)
     fused = api.profile_collect("pack_sgd")["launches"]
+    fused_bytes = api.profile_collect("pack_sgd")["bytes"]
     packs = api.profile_collect("pack")["launches"]
     w = m.read_weights()
     m.close()
@@ -42,6 +47,55 @@ def test_fused_pack_update_matches_oracle(gpu, wdt, gdt, cdt, mu, bucket_bytes):
     np.testing.assert_array_equal(w, exp)
     assert np.max(np.abs(w.astype(np.float64) - r64) / sc) <= (1e-2 if "bf16" in (gdt, cdt) else 1e-6)
     assert fused == 3 * nb and packs == 0, (fused, packs)
+    if direct and gdt == cdt:  # no staging store: the bucket bytes are not moved
+        es = {"f64": 8, "f32": 4, "bf16": 2}
+        per = es[gdt] + 2 * es[wdt] + (2 * (8 if wdt == "f64" else 4) if mu else 0)
+        assert fused_bytes == pytest.approx(3 * sum(SIZES) * per), fused_bytes
+
+
+def test_registered_gradients_are_not_staged(gpu):
+    """With registered gradients the one-rank fused pull_update reads them
+    in place and writes nothing into the comm bucket (documented: the buckets
+    then hold no copy of those gradients, as under ZeRO-1), while the weights
+    are the staged run's."""
+    from paper_1802_06949_b200 import Engine, KvConfig, KvStore, Slot, Transport
+    K = len(SIZES)
+    res = {}
+    for reg in (False, True):
+        tr = Transport.local(1, 10000)
+        eng = Engine(2, 0, None, 0)
+        offs, o = [], 0
+        for n in SIZES:
+            offs.append(o)
+            o += (n * 4 + 255) // 256 * 256
+        arena = torch.zeros(o // 4, dtype=torch.float32, device="cuda")
+        store = KvStore(eng, tr, 0, KvConfig("depcha", 1, K, bucket_bytes=1 << 20, issue_order=1))
+        ws = [Slot(torch.from_numpy(O.random_uniform(n, O.mix_seed(7, k)).astype(np.float32)).cuda(),
+                   eng.new_variable()) for k, n in enumerate(SIZES)]
+        gs = []
+        for k, n in enumerate(SIZES):
+            g = arena[offs[k] // 4:offs[k] // 4 + n]
+            g.copy_(torch.from_numpy(O.random_uniform(n, 1000 + k).astype(np.float32)))
+            gs.append(Slot(g, eng.new_variable()))
+        for k in range(K):
+            store.init(k, ws[k])
+        eng.wait_all()
+        if reg:
+            store.register_grads(arena.data_ptr(), arena.numel() * 4)
+        for _ in range(2):
+            store.push(list(range(K)), gs)
+            store.pull_update(list(range(K)), ws, 0.1, 1.0 / 64, 0.9)
+        eng.wait_all()
+        res[reg] = ([w.value.cpu().numpy() for w in ws], store.comm_buf(3))
+        store.close()
+        eng.close()
+        tr.close()
+    for a, b in zip(res[False][0], res[True][0]):
+        np.testing.assert_array_equal(a, b)
+    g3 = O.random_uniform(SIZES[3], 1003).astype(np.float32)
+    np.testing.assert_array_equal(res[False][1], g3)  # staged: the bucket holds the gradient
+    # registered: the bucket keeps what init's broadcast left there, not the gradient
+    assert not np.array_equal(np.asarray(res[True][1]), g3), "registered gradients must not be staged"
 
 
 def test_other_uses_of_the_bucket_see_the_staged_gradient(gpu):
@@ -102,7 +156,7 @@ def test_e2e_host_upload_gives_the_device_run_weights(gpu, R):
         try:
             eng = Engine(4, r, None, 0)
             kw = dict(mode="depcha", bucket_bytes=1 << 20, issue_order=1, lr=0.1, rescale=1.0 / 64, momentum=0.9,
-                      p2p=R > 1, zero=R > 1, direct_grads=R > 1)
+                      p2p=R > 1, zero=R > 1, direct_grads=True)
             m1 = api.SynthModel(eng, tr, r, R, sizes, host_source=True, **kw)
             m1.init()
             m1.run_e2e(5, m1.BACKWARD | m1.COMM)
