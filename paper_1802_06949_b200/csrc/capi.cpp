@@ -175,8 +175,8 @@ int cs_trace_write_jsonl(cs_trace_t t, const char* path) {
 int cs_trace_gauges(cs_trace_t t, int* max_open, int* overlap) {
   return guard([&] {
     CHECK_HANDLE(t);
-    *max_open = t->sink.gauges().max_open_collectives.load();
-    *overlap = t->sink.gauges().compute_overlap.load() ? 1 : 0;
+    *max_open = t->sink.gauges().max_open_collectives();
+    *overlap = t->sink.gauges().compute_overlap() ? 1 : 0;
   });
 }
 
