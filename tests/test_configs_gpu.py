@@ -41,6 +41,7 @@ def run_config(keys, R, *, mode, dtype, bucket_mb, peer, outstanding=1, zero=Fal
                                comm_dtype=D[dtype], bucket_bytes=int(bucket_mb * 2**20), issue_order=1,
                                outstanding=outstanding, lr=0.1, rescale=1.0 / (64 * R), momentum=momentum,
                                p2p=1 if peer else 0, zero=zero, order_seed=order_seed,
+                               direct_grads=mode != "concom",  # the bench default: registered gradients
                                concom_comms=comms)
             m.init()
             m.run(3, m.BACKWARD | m.COMM)
