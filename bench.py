@@ -59,7 +59,9 @@ CONFIGS = {
     "alexnet": ("alexnet", "concom", 4, "fp32", 25, "alexnet_b64_amp.json"),
     "resnet152": ("resnet152", "depcha", 1, "bf16", 128, "resnet152_b64_amp.json"),
     "inception_v3": ("inception_v3", "depcha", 1, "bf16", 128, 30.0),
-    "stress": ("stress", "depcha", 1, "fp32", 64, 0.0),
+    # 256 MiB buckets: 51 launches per step instead of 236 (64 MiB measured
+    # slower and, at 2 GPUs, multimodal: profiles/r2_stress_buckets.log)
+    "stress": ("stress", "depcha", 1, "fp32", 256, 0.0),
     "uniform16": ("uniform16x1048576", "funnel", 1, "fp32", 0, 0.0),
 }
 CALIB = ROOT / "paper_1802_06949_b200" / "calibration"
