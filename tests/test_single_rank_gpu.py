@@ -183,3 +183,32 @@ def test_e2e_host_upload_gives_the_device_run_weights(gpu, R):
     for r in range(R):
         np.testing.assert_array_equal(out[r][0], out[r][1])
         np.testing.assert_array_equal(out[r][0], out[0][0])
+
+
+def test_bench_inputs_are_the_reference_generator():
+    """The bench's synthetic inputs (SynthModel: trainer.cpp fill_uniform) are
+    the reference's random_uniform (tensor.cpp:28-38) with mix_seed
+    (tensor.cpp:76-81) -- checked value for value, not only through the
+    weights they produce: weights straight after init (rank 0's, seeds
+    mix_seed(7, k)), then one plain fp64 SGD step, bit-exact against the
+    oracle's update of the reference-generated gradients (seeds 1000 + k)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs cuda:0")
+    from paper_1802_06949_b200 import Engine, Transport, api
+    sizes = [1, 7, 64, 300, 4097]
+    tr = Transport.local(1, 10000)
+    eng = Engine(2, 0, None, 0)
+    m = api.SynthModel(eng, tr, 0, 1, sizes, mode="depcha", w_dtype=api.F64, g_dtype=api.F64, comm_dtype=api.F64,
+                       bucket_bytes=1 << 20, issue_order=1, lr=1.0, rescale=1.0 / 128, momentum=0.0)
+    m.init()
+    w0 = m.read_weights()
+    m.run(1, m.BACKWARD | m.COMM)
+    w1 = m.read_weights()
+    m.close()
+    eng.close()
+    tr.close()
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for k, n in enumerate(sizes):
+        np.testing.assert_array_equal(w0[offs[k]:offs[k + 1]], O.random_uniform(n, O.mix_seed(7, k)))
+        exp, _ = O.sgd_update(O.random_uniform(n, O.mix_seed(7, k)), O.random_uniform(n, 1000 + k), 1.0, 1.0 / 128)
+        np.testing.assert_array_equal(w1[offs[k]:offs[k + 1]], exp)

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--staged", action="store_true", help="stage the gradients (no register_grads)")
     ap.add_argument("--replicated", action="store_true", help="replicated update instead of ZeRO-1")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--keyset", default="resnet50")
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--bucket-mb", type=float, default=100)
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -41,8 +44,10 @@ def main():
     dist.broadcast_object_list(name, src=0)
     tr = api.Transport.nccl(name[0], world, rank, local, 60000)
     eng = api.Engine(4, rank, None, local)
-    keys = keysets.load("resnet50")
-    m = api.SynthModel(eng, tr, rank, world, keys, mode="depcha", bucket_bytes=100 << 20, issue_order=1, lr=0.1,
+    keys = keysets.load(a.keyset)
+    dt = {"fp32": api.F32, "bf16": api.BF16}[a.dtype]
+    m = api.SynthModel(eng, tr, rank, world, keys, mode="depcha", g_dtype=dt, comm_dtype=dt,
+                       bucket_bytes=int(a.bucket_mb * 2**20), issue_order=1, lr=0.1,
                        rescale=1.0 / (64 * world), momentum=0.9, p2p=1, zero=not a.replicated,
                        direct_grads=not a.staged)
     m.init()
@@ -67,7 +72,8 @@ def main():
     out = [None] * world
     dist.all_gather_object(out, summary)
     if rank == 0:
-        print(json.dumps({"tool": "p2ptrace", "world": world, "gradients": "staged" if a.staged else "direct",
+        print(json.dumps({"tool": "p2ptrace", "world": world, "keyset": a.keyset, "dtype": a.dtype,
+                          "gradients": "staged" if a.staged else "direct",
                           "update": "replicated" if a.replicated else "zero1", "ranks": out}))
     m.close()
     eng.close()
