@@ -517,6 +517,11 @@ Dispatch KvStore::depcha_dispatch() const {
     return e && std::string(e) == "pool";
   }();
   if (cfg_.mode == KvMode::Naive || pool) return Dispatch::Pool;
+  // an injected latency makes every collective block its dispatching host
+  // thread (the reference's blocking MPI call, collective.cpp:249): then the
+  // collectives belong on the pool, as in the reference (kvstore.cpp:163-179),
+  // so the control thread keeps issuing the next step (acceptance 7)
+  if (transport_.inject_latency().count() > 0) return Dispatch::Pool;
   return Dispatch::Inline;
 }
 

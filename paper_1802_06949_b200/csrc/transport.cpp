@@ -514,6 +514,7 @@ int Transport::new_communicator() {
 }
 
 void Transport::set_inject_latency(std::chrono::microseconds us) { ledger_->set_inject_latency(us); }
+std::chrono::microseconds Transport::inject_latency() const { return ledger_->inject_latency(); }
 
 void Transport::abort(const std::string& why) {
   // release every peer kernel still waiting in a pair barrier (they poll

@@ -68,6 +68,7 @@ class Transport {
   void barrier(int comm, int rank, int trace_key, cudaStream_t stream);
 
   void set_inject_latency(std::chrono::microseconds us);
+  std::chrono::microseconds inject_latency() const;
   void abort(const std::string& why);
   Ledger& ledger() { return *ledger_; }
 
