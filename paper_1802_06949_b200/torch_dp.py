@@ -16,9 +16,9 @@ the producer is PyTorch autograd on its own CUDA stream:
   the bucket (shard_only; the rest still holds this rank's own gradient), and
   with ``zero=True`` no sum at all (the reduction stays in registers).  Code
   that reads p.grad after step() (clipping, logging) must read it before
-  step() or run with ``p2p=0``.  At world > 1 over the peer-memory kernel the
-  arena is registered (``direct_grads``, KvStore.register_grads): the fused
-  kernel reads every rank's gradients in place, so push stages nothing;
+  step() or run with ``p2p=0``.  The arena is registered (``direct_grads``,
+  KvStore.register_grads; at world > 1 with the peer-memory kernel): the
+  fused kernels read the gradients in place, so push stages nothing;
 * a post-accumulate-grad hook counts ready gradients per fusion bucket; when a
   bucket is complete it records a CUDA event on the autograd stream,
   ``Engine.import_event`` turns it into the latest write of the gradients
@@ -98,9 +98,10 @@ class TorchKvStoreDP:
         torch.cuda.synchronize(dev)  # the weights were written on the framework stream
         for k in range(K):
             self.kv.init(k, self.w_slots[k])  # rank 0's weights broadcast (kvstore.cpp:95)
-        if direct_grads and not bucket_views and world > 1 and p2p == 1:
-            # the flat arena is registered (a setup collective): the fused peer
-            # kernel reads every rank's gradients in place, nothing is staged
+        if direct_grads and not bucket_views and (world == 1 or p2p == 1):
+            # the flat arena is registered (a setup collective): the fused
+            # kernels read the gradients in place (every rank's over NVLink at
+            # world > 1), nothing is staged into the comm buckets
             self.kv.register_grads(self.grad_arena.data_ptr(), self.grad_arena.numel() * esz)
         # gradient-ready groups = fusion buckets (built here, identically on every rank)
         groups: dict[int, list[int]] = {}
