@@ -7,11 +7,17 @@
 //                        (collective.cpp:228-236: acc = b0; acc += b1 ...; copy to all)
 //   (c) cs_sgd_update  : fused unpack + rescale + SGD / momentum update
 //                        (model.cpp:17-27, trainer.cpp:74-80)
+//   pack_sgd_tab_kernel: (a)+(c) fused for one rank (the allreduce between
+//                        them is the identity): DepCha's whole step in one
+//                        launch; registered gradients skip the staging store
 //   p2p_allreduce_kernel / p2p_zero_kernel
 //                      : (b)+(c) fused over CUDA-IPC peer memory or an NVSwitch
 //                        multicast VA, one cooperative launch per bucket,
 //                        rank-order sums, pair barriers per CTA; the ZeRO-1
-//                        form updates a sharded master and all-gathers weights
+//                        form updates a sharded master and all-gathers weights;
+//                        gradients staged in-kernel or read in place from every
+//                        rank's registered region (direct); optional per-CTA
+//                        phase stamps (CSB_P2P_TRACE)
 //   cs_synth_backward  : synthetic per-key backward producer (bench only)
 //   cs_checksum        : deterministic fp64 checksum (e2e result read-back)
 //
@@ -21,16 +27,18 @@
 // DeviceTable.
 //
 // Design of the streaming kernels (B200, HBM-bound, no tensor cores):
-//   * 256-thread CTAs; a thread moves groups of 8 elements as 16-byte
-//     vectors (ld/st .v4 / .v2.f64), 2-4 groups unrolled with every load
-//     issued before the first store (>= 64 B in flight per thread).
-//   * A launch covers a whole table of keys (one bucket): per-entry group
-//     prefix sums, pointers and sizes travel in a __grid_constant__
-//     kernel-parameter block (<= 21 KB, constant bank), so no host->device
-//     copy precedes a launch; a CTA finds its first entry by binary search.
-//   * Grid = exactly one wave (148 SMs x occupancy of the instantiation);
-//     the table's groups are split evenly over it, so every CTA moves the
-//     same bytes and there is no tail wave.
+//   * 256-thread CTAs, one wave (148 SMs x resident CTAs); work in chunks of
+//     256 x U 8-element groups dealt round-robin to the CTAs (for_chunks),
+//     the last partial round split over every CTA; inside a chunk each lane
+//     moves 16-byte slots lane-contiguously, every load of the chunk issued
+//     before its first store.
+//   * A launch covers a whole table of keys (one bucket): the entries live
+//     in a device-resident table (DeviceTable, re-uploaded only when an entry
+//     changes) with each chunk's first entry precomputed, or -- for the
+//     one-off C-ABI launches -- in a __grid_constant__ parameter block.
+//   * Streaming data moves with evict-first global loads / stores (LDG/STG
+//     .EF.128 in SASS); the one-rank kernel is launched with programmatic
+//     dependent launch.
 //   * Arithmetic uses explicit round-to-nearest intrinsics (__dmul_rn,
 //     __fsub_rn, ...) so nothing is contracted into an FMA: fp64 results are
 //     bit-identical to the reference, fp32 to the oracle's fp32 restatement.
