@@ -2172,8 +2172,8 @@ void p2p_allreduce(const P2PArgs& a, cudaStream_t s) {
     if (!aligned16(a.wm[r])) throw UsageError("p2p_allreduce: master shard not 16-byte aligned");
   }
   p.mom_b = a.mom_b;
-  p.direct = (a.direct && a.update && a.tab && a.n_entries > 0 && !a.mc) ? 1 : 0;
-  if (a.direct && !p.direct) throw UsageError("p2p_allreduce: direct gradient reads need the fused update over peer memory");
+  p.direct = (a.direct && a.tab && a.n_entries > 0 && !a.mc) ? 1 : 0;
+  if (a.direct && !p.direct) throw UsageError("p2p_allreduce: direct gradient reads need the key table over peer memory");
   for (int r = 0; p.direct && r < a.nranks; ++r) {
     p.gbase[r] = a.gbase[r];
     if (!aligned16(a.gbase[r])) throw UsageError("p2p_allreduce: gradient region not 16-byte aligned");

@@ -399,7 +399,11 @@ void KvStore::push(const std::vector<int>& keys, const std::vector<TensorSlot>& 
       keys_[static_cast<size_t>(k)].pushed = true;
     }
     const int key0 = keys[static_cast<size_t>(idxs[0])];
-    if (defer_pack_ && (B.deferred_dt < 0 || B.deferred_dt == src_dt)) {
+    // Funnel over peer memory with registered gradients: defer too -- the
+    // bucket's collective reads the gradients in place if they all lie in
+    // the region (issue_collective), else flushes the pack first
+    const bool funnel_direct = p2p_active_ && cfg_.mode == KvMode::Funnel && !greg_peers_.empty();
+    if ((defer_pack_ || funnel_direct) && (B.deferred_dt < 0 || B.deferred_dt == src_dt)) {
       // one rank: stage at the pull_update, fused with the update (or flushed
       // as this very pack op by any other use of the bucket)
       size_t j = 0;
@@ -465,8 +469,47 @@ void KvStore::issue_collective(int b, const std::vector<Tag>& extra_reads) {
     // control-thread collective on the single ordered comm stream
     // (kvstore.cpp:112-116); the funnel tag keeps issue order = push order
     muts.push_back(funnel_tag_);
-    engine_.push_stream([self, b](cudaStream_t s) { self->collective_body(self->buckets_[b], b, s, nullptr); },
-                        {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+    // registered gradients: the peer kernel reads every rank's gradients in
+    // place and writes the sums into every bucket -- no pack (§7.2)
+    const bool direct = p2p_active_ && B.view_tags.empty() && B.deferred.size() == B.keys.size() &&
+                        (B.deferred_dt < 0 || B.deferred_dt == comm_dt_) && deferred_in_region(B);
+    if (!direct) flush_deferred(B);
+    if (direct) {
+      std::vector<DeviceTable::Entry> es;
+      for (const auto& [k, e] : B.deferred) {
+        const KeyState& ks = keys_[static_cast<size_t>(k)];
+        const uint64_t g0 = ks.offset / 8;
+        DeviceTable::Entry en{key_ptr(k), nullptr, nullptr, e.n, g0, g0 + (e.n + 7) / 8};
+        en.d = const_cast<void*>(e.src);
+        es.push_back(en);
+      }
+      std::sort(es.begin(), es.end(), [](const auto& x, const auto& y) { return x.gstart < y.gstart; });
+      uint64_t layout = 1469598103934665603ull;  // FNV-1a of (slot, region offset), as the fused pull
+      for (const auto& e : es)
+        for (uint64_t v : {e.gstart, static_cast<uint64_t>(static_cast<const char*>(e.d) -
+                                                           static_cast<const char*>(greg_base_))}) {
+          layout ^= v;
+          layout *= 1099511628211ull;
+        }
+      std::vector<Tag> reads = B.deferred_reads;
+      clear_deferred(B);
+      if (!B.p2p_tab) B.p2p_tab = std::make_shared<DeviceTable>();
+      DeviceTable* ptab = B.p2p_tab.get();
+      engine_.push_stream(
+          [self, b, es, ptab, layout](cudaStream_t s) {
+            Transport::P2PUpdate u;
+            u.update = false;  // a plain allreduce of the in-place gradients into the buckets
+            u.tab = ptab->resident(es, s);
+            u.n_entries = static_cast<int>(es.size());
+            u.gbase = self->greg_peers_.data();
+            u.layout = layout;
+            self->collective_body(self->buckets_[b], b, s, &u);
+          },
+          reads, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+    } else {
+      engine_.push_stream([self, b](cudaStream_t s) { self->collective_body(self->buckets_[b], b, s, nullptr); },
+                          {}, muts, OpKind::Collective, key0, B.lane, Dispatch::Inline);
+    }
     // The funnel: ONE thread performs every collective, synchronously.  The
     // reference's push waits for the gradient and runs the allreduce on the
     // calling (control) thread (kvstore.cpp:112-116), so nothing after it --

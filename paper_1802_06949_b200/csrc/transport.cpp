@@ -371,8 +371,9 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   sig.count = static_cast<int64_t>(count);
   // every rank must run the same barrier protocol (a shard_only
   // rank would wait at a phase-2 barrier its peers never reach)
-  sig.variant = kVarP2P | (mc ? kVarNvls : 0) | (upd ? kVarUpdate : 0) |
-                (upd && upd->shard_only && !mc ? kVarShardOnly : 0) | (upd && upd->wm ? kVarZero : 0) |
+  const bool fused = upd && upd->update;
+  sig.variant = kVarP2P | (mc ? kVarNvls : 0) | (fused ? kVarUpdate : 0) |
+                (fused && upd->shard_only && !mc ? kVarShardOnly : 0) | (fused && upd->wm ? kVarZero : 0) |
                 (upd && upd->gbase && !mc ? kVarDirect : 0);
   if (sig.variant & kVarDirect) sig.layout = upd->layout;
   Ledger::Ticket t;
@@ -401,7 +402,7 @@ void Transport::allreduce_p2p(int comm, int rank, void* const* peer_bufs, uint64
   a.cdt = dtype;
   a.epoch = static_cast<uint32_t>(t.seq + 1);  // same matched sequence on every rank
   if (upd) {
-    a.update = true;
+    a.update = upd->update;
     a.tab = upd->tab;
     a.n_entries = upd->n_entries;
     a.wdt = upd->wdt;

@@ -98,6 +98,7 @@ class Transport {
   struct P2PUpdate {
     const DeviceTable::Entry* tab = nullptr;  // bucket-group coordinates, sorted
     int n_entries = 0;
+    bool update = true;  // false: a plain allreduce (the table only locates direct-read gradients)
     int wdt = CS_F32;
     double lr = 0, rescale = 0, momentum = 0;
     bool shard_only = false;  // the bucket keeps only this rank's shard (update reads owners)

@@ -196,9 +196,10 @@ def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False, shared_c
         sizes = [1, 7, 64, 300, 4097, 70000, 1 << 18]
         K = len(sizes)
         res = {}
-        variants = ([(z, g, d) for z in (0, 1) for g in (api.F32, api.BF16) for d in (0, 1)]
-                    if case == "direct" else [(1, api.F32, 1)])
-        for zero, gdt, direct in variants:
+        variants = ([("depcha", z, g, d) for z in (0, 1) for g in (api.F32, api.BF16) for d in (0, 1)] +
+                    [("funnel", 0, g, d) for g in (api.F32, api.BF16) for d in (0, 1)]
+                    if case == "direct" else [("depcha", 1, api.F32, 1)])
+        for mode, zero, gdt, direct in variants:
             tdt, esz = (torch.float32, 4) if gdt == api.F32 else (torch.bfloat16, 2)
             shift = 256 * rank if case == "direct_mismatch" else 0
             offs, o = [], shift
@@ -207,7 +208,7 @@ def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False, shared_c
                 o += (n * esz + 255) // 256 * 256
             garena = torch.zeros(o, dtype=torch.uint8, device=dev)
             eng = Engine(4, rank, None, local)
-            store = KvStore(eng, tr, rank, KvConfig("depcha", 1, K, comm_dtype=gdt, bucket_bytes=256 * 1024,
+            store = KvStore(eng, tr, rank, KvConfig(mode, 1, K, comm_dtype=gdt, bucket_bytes=256 * 1024,
                                                     issue_order=1, p2p=1, zero=zero))
             ws = [Slot(torch.from_numpy(np.ascontiguousarray(
                 O.random_uniform(n, O.mix_seed(7, k)) if rank == 0 else np.zeros(n), dtype=np.float32)).to(dev),
@@ -231,8 +232,9 @@ def run_rank(case, rank, world, tr, dev, outdir, sink, colocated=False, shared_c
             except MismatchError as e:
                 out["error"] = type(e).__name__ + ": " + str(e)
             if out.get("error") is None:
+                tag = "" if mode == "depcha" else "f"
                 for k in range(K):
-                    res[f"z{zero}_g{gdt}_d{direct}_k{k}"] = ws[k].value.cpu().numpy()
+                    res[f"{tag}z{zero}_g{gdt}_d{direct}_k{k}"] = ws[k].value.cpu().numpy()
             store.close()
             eng.close()
         np.savez(outdir / f"{case}_r{rank}.npz", **res)

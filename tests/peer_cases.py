@@ -128,12 +128,13 @@ def check_zero_vs_oracle(d: Path, R: int):
 
 def check_direct(d: Path, R: int):
     """Direct gradient reads (registered region, nothing staged) give the
-    staged run's weights bit for bit -- ZeRO-1 and replicated, fp32 and bf16
-    gradients -- on every rank, and the fp32 ZeRO-1 run equals the f32 oracle."""
+    staged run's weights bit for bit -- DepCha's fused ZeRO-1 and replicated
+    kernels and Funnel's plain allreduce, fp32 and bf16 gradients -- on every
+    rank, and the fp32 ZeRO-1 run equals the f32 oracle."""
     outs = [np.load(d / f"direct_r{r}.npz") for r in range(R)]
     for r in range(R):
         names = [n for n in outs[r].files if "_d1_" in n]
-        assert len(names) == 4 * 7, names
+        assert len(names) == 6 * 7, names  # DepCha: ZeRO-1 / replicated x fp32 / bf16; Funnel: fp32 / bf16
         for name in names:
             np.testing.assert_array_equal(outs[r][name], outs[r][name.replace("_d1_", "_d0_")],
                                           err_msg=f"R={R} rank {r} {name}")
